@@ -1,0 +1,96 @@
+"""Pin the CPU oracle (oracle/aqr_oracle.c) to the reference's own outputs.
+
+The fixtures in tests/golden/ were produced by the reference package itself
+(tests/golden/make_golden.py imports /root/reference/pkg/src/aqr).  The
+oracle restates _gs_factor (gram_schmidt.py:126-179) with the same
+sequential-accumulation contract (_kernels_impl.py:1-12), so every check
+here is BITWISE.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+GS_METHODS = [f"{f}-{v}-{o}" for f in ("mgs", "cgs") for v in ("naive", "ha", "hp")
+              for o in ("col", "row")]
+
+
+def _op(g, key):
+    if f"{key}|A" in g:
+        return ("dense", g[f"{key}|A"])
+    return ("csr", g[f"{key}|indptr"], g[f"{key}|indices"], g[f"{key}|data"])
+
+
+KEYS = ["hand", "dense0", "dense1", "dense2", "dense3", "dense7", "ident", "illcond",
+        "csr9x7", "csr16"]
+
+
+@pytest.mark.parametrize("key", KEYS)
+@pytest.mark.parametrize("method", GS_METHODS)
+def test_oracle_bitwise_equals_reference(golden, key, method):
+    if f"{key}|{method}|Q" not in golden and f"{key}|{method}|breakdown" not in golden:
+        pytest.skip("method not in fixture")
+    Z = golden[f"{key}|Z"]
+    op = _op(golden, key)
+    if f"{key}|{method}|breakdown" in golden:
+        col, val = golden[f"{key}|{method}|breakdown"]
+        with pytest.raises(O.OracleBreakdown) as info:
+            O.gs_factor(Z, op, method)
+        assert info.value.column == int(col)
+        return
+    r = O.gs_factor(Z, op, method)
+    assert np.array_equal(r.Q, golden[f"{key}|{method}|Q"])
+    assert np.array_equal(r.R, golden[f"{key}|{method}|R"])
+    assert r.flagged_columns == golden[f"{key}|{method}|flag"].tolist()
+    assert r.mv_count == int(golden[f"{key}|{method}|mv"][0])
+
+
+def test_hand_instance_exact(golden):
+    # test_gram_schmidt.py:66-77: all arithmetic exact in binary64
+    for meth in GS_METHODS:
+        r = O.gs_factor(golden["hand|Z"], ("dense", golden["hand|A"]), meth)
+        assert np.array_equal(r.Q, [[1.0, 0.0], [0.0, 0.5]])
+        assert np.array_equal(r.R, [[1.0, 1.0], [0.0, 2.0]])
+
+
+def test_breakdown_kat(golden_cases):
+    Z = np.array([[1.0, 2.0], [0.0, 0.0], [0.0, 0.0]])
+    for meth, expect in golden_cases["breakdown_rank_deficient"].items():
+        with pytest.raises(O.OracleBreakdown) as info:
+            O.gs_factor(Z, ("dense", np.eye(3)), meth)
+        assert [info.value.column, info.value.value] == expect
+
+
+def test_flag_kat(golden_cases):
+    for meth, expect in golden_cases["flag_tiny_norm"].items():
+        r = O.gs_factor(np.array([[1.0], [1e-16]]), ("dense", np.diag([1e-30, 1.0])), meth)
+        assert r.flagged_columns == expect["flagged"] == [0]
+        assert r.R[0, 0] == expect["R00"] > 0
+        assert r.Q.ravel().tolist() == expect["Q"]
+
+
+def test_seq_dot_vs_fsum():
+    # test_backends.py:139-145
+    rng = np.random.default_rng(12345)
+    x, y = rng.standard_normal(1000), rng.standard_normal(1000)
+    exact = math.fsum(float(a) * float(b) for a, b in zip(x, y))
+    assert O.seq_dot(x, y) == pytest.approx(exact, rel=1e-12)
+
+
+def test_cfg1_inputs_and_outputs_pinned(golden_cases, golden):
+    import cfg1
+
+    A, Z = cfg1.make()
+    c1 = golden_cases["cfg1"]
+    assert cfg1.sha(A) == c1["A_sha"]
+    assert cfg1.sha(Z) == c1["Z_sha"]
+    for meth, ref in c1["methods"].items():
+        r = O.gs_factor(Z, ("dense", A), meth)
+        assert cfg1.sha(r.Q) == ref["Q_sha"], meth
+        assert cfg1.sha(r.R) == ref["R_sha"], meth
+        assert np.array_equal(r.R, golden[f"cfg1|{meth}|R"])
+        assert r.flagged_columns == ref["flagged"]
+        assert r.mv_count == ref["mv_count"]
