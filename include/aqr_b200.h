@@ -1,0 +1,228 @@
+/*
+ * aqr_b200.h -- C ABI of libaqr_b200.so, the B200 (sm_100a) implementation of
+ * the A-orthogonal modified Gram-Schmidt hot path of the reference package
+ * `aqr` (arXiv 1703.10440).
+ *
+ * Conventions (all entry points):
+ *   - plain pointers and sizes only; no torch/C++ types cross this boundary;
+ *   - every double* / int32_t* argument is a DEVICE pointer unless the name
+ *     ends in _host;
+ *   - matrices are column-major (Fortran) with an explicit leading dimension,
+ *     the layout aqr.operators.as_matrix produces (operators.py:28-33);
+ *   - work is enqueued on the caller's `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream); nothing allocates on the hot path
+ *     except the *_host convenience entry, which owns its device buffers;
+ *   - every function returns an aqr_status; aqr_last_error() describes the
+ *     last failure on the calling thread.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/aqr):
+ *   aqr_gs_factor / aqr_gs_factor_host  <- gram_schmidt._gs_factor (126-179),
+ *       reached by mgs_naive/mgs_ha/mgs_hp/cgs/factorize (182-206, 227-233)
+ *   aqr_op (+ callbacks)                <- operators.SpdOperator.apply /
+ *       apply_block plug-in point (operators.py:43-73), DenseSpdOperator
+ *       (76-93), CsrSpdOperator (96-129)
+ *   aqr_dot / aqr_sub_scaled / aqr_div_scalar / aqr_matvec /
+ *   aqr_apply_block_dense / aqr_csr_matvec <- the kernel namespace returned
+ *       by backend.kernels() (backend.py:66-68): seq_dot, sub_scaled,
+ *       div_scalar, matvec, apply_block_dense, csr_matvec
+ *       (_kernels_impl.py:17-56, 85-93)
+ *   aqr_step_*                          <- the bodies of _gs_factor's
+ *       project(i, j) (139-145) and normalize(j) (147-165), restated as the
+ *       fused one-pass-per-step schedule used by the multi-GPU driver.
+ */
+#ifndef AQR_B200_H
+#define AQR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AQR_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define AQR_API __attribute__((visibility("default")))
+#else
+#define AQR_API
+#endif
+
+typedef enum {
+    AQR_OK = 0,
+    AQR_EDIM = 1,       /* DimensionError (gram_schmidt.py:116-123)            */
+    AQR_EBREAKDOWN = 2, /* BreakdownError(column, value) (gram_schmidt.py:153) */
+    AQR_ECUDA = 3,      /* CUDA runtime / launch failure                       */
+    AQR_EARG = 4,       /* bad enum, null pointer, size out of range           */
+    AQR_ENOMEM = 5,     /* workspace too small / device allocation failed      */
+    AQR_ECALLBACK = 6   /* a user operator callback returned non-zero          */
+} aqr_status;
+
+typedef enum { AQR_MGS = 0, AQR_CGS = 1 } aqr_family;           /* MethodId.family  */
+typedef enum { AQR_NAIVE = 0, AQR_HA = 1, AQR_HP = 2 } aqr_variant; /* MethodId.variant */
+typedef enum { AQR_COL = 0, AQR_ROW = 1 } aqr_orientation;      /* MethodId.orientation */
+
+typedef enum {
+    AQR_OP_DENSE = 0,   /* DenseSpdOperator: A m x m column-major, lda >= m   */
+    AQR_OP_CSR = 1,     /* CsrSpdOperator: int32 indptr/indices, fp64 data    */
+    AQR_OP_CALLBACK = 2 /* user operator: apply/apply_block callbacks         */
+} aqr_op_kind;
+
+/* Y[:, 0:k] = A X[:, 0:k] on `stream`; return 0 on success.  k == 1 is
+ * SpdOperator.apply, k > 1 SpdOperator.apply_block. */
+typedef int (*aqr_apply_fn)(void *ctx, int64_t k, const double *X, int64_t ldx, double *Y,
+                            int64_t ldy, void *stream);
+
+typedef struct aqr_op {
+    int32_t kind; /* aqr_op_kind */
+    int32_t spmv_lanes; /* CSR: lanes cooperating on one row (1..32, 0 = auto) */
+    int64_t m;
+    /* AQR_OP_DENSE */
+    const double *A;
+    int64_t lda;
+    /* AQR_OP_CSR (nnz < 2^31) */
+    const int32_t *indptr;
+    const int32_t *indices;
+    const double *data;
+    int64_t nnz;
+    /* AQR_OP_CALLBACK */
+    aqr_apply_fn apply;       /* called with k == 1                      */
+    aqr_apply_fn apply_block; /* called with k == n (HP); may equal apply */
+    void *ctx;
+} aqr_op;
+
+/* Everything _gs_factor takes and returns.  Inputs above the marker. */
+typedef struct aqr_factor_args {
+    int32_t family, variant, orientation;
+    int32_t reserved;
+    int64_t m, n;
+    const double *Z; /* m x n, ldz; may alias Q (then factorized in place) */
+    int64_t ldz;
+    double *Q; /* m x n output, ldq */
+    int64_t ldq;
+    double *R; /* n x n output, ldr; strict lower part set to 0.0 */
+    int64_t ldr;
+    const aqr_op *op;
+    void *workspace; /* device, >= aqr_workspace_bytes(...) bytes, 256-B aligned */
+    uint64_t workspace_bytes;
+    /* ---- outputs (host memory) ---- */
+    int64_t fail_col;        /* -1, or the BreakdownError column           */
+    double fail_val;         /* the offending z'Az                          */
+    int64_t mv_count;        /* operator applications performed (built-in ops) */
+    int32_t *flagged_host;   /* optional: n entries, 1 where column flagged */
+} aqr_factor_args;
+
+/* ---- whole factorization (the drop-in for _gs_factor) ------------------ */
+
+AQR_API uint64_t aqr_workspace_bytes(int32_t family, int32_t variant, int32_t orientation, int64_t m,
+                             int64_t n);
+
+/* Runs the full factorization on `stream`, then synchronizes it to read the
+ * breakdown/flag record (one small D2H copy).  AQR_EBREAKDOWN leaves Q/R
+ * undefined, as the reference raises without a partial result. */
+AQR_API aqr_status aqr_gs_factor(aqr_factor_args *args, void *stream);
+
+/* Same, with HOST Z/Q/R (column-major, ld = m / m / n) and a host-side
+ * operator description (dense A, or CSR with int64 indptr/indices as the
+ * reference's CsrSpdOperator holds them, operators.py:100-101).  Owns all
+ * device memory; H2D of inputs and D2H of Q/R happen inside the call. */
+AQR_API aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientation, int64_t m,
+                              int64_t n, const double *Z_host, double *Q_host, double *R_host,
+                              int32_t op_kind, const double *A_host, const int64_t *indptr_host,
+                              const int64_t *indices_host, const double *data_host, int64_t nnz,
+                              int64_t *fail_col, double *fail_val, int32_t *flagged_host,
+                              int64_t *mv_count);
+
+/* ---- operator kernels (SpdOperator realizations) ---------------------- */
+
+/* Y = A X for k columns.  Each output entry accumulates strictly in the
+ * reference order (dense: ascending column index, _kernels_impl.py:24-47;
+ * CSR: stored order, :50-56) with separately rounded multiply and add, so
+ * the results are bitwise equal to the reference's matvec / csr_matvec. */
+AQR_API aqr_status aqr_op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                        int64_t ldy, void *stream);
+
+/* ---- the reference kernel namespace (backend.kernels()) ---------------- */
+
+/* out[0] = x . y  (deterministic tree reduction; device scalar out)       */
+AQR_API aqr_status aqr_dot(int64_t m, const double *x, const double *y, double *out, void *stream);
+/* z -= a * q with a read from device memory a_dev[0] (no FMA contraction) */
+AQR_API aqr_status aqr_sub_scaled(int64_t m, double *z, const double *a_dev, const double *q,
+                          void *stream);
+/* out = x / r_dev[0] (IEEE division)                                      */
+AQR_API aqr_status aqr_div_scalar(int64_t m, const double *x, const double *r_dev, double *out,
+                          void *stream);
+AQR_API aqr_status aqr_matvec(int64_t m, const double *A, int64_t lda, const double *x, double *y,
+                      void *stream);
+AQR_API aqr_status aqr_apply_block_dense(int64_t m, int64_t k, const double *A, int64_t lda,
+                                 const double *X, int64_t ldx, double *Y, int64_t ldy,
+                                 void *stream);
+AQR_API aqr_status aqr_csr_matvec(int64_t m, const int32_t *indptr, const int32_t *indices,
+                          const double *data, const double *x, double *y, void *stream);
+
+/* ---- step kernels (one MGS step of the row-oriented fused schedule) ----
+ * Used by the multi-GPU driver, which inserts its NCCL all-reduces between
+ * *_partials and *_finish.  `ntiles` = aqr_num_tiles(m_local).
+ * Rt is the n x n R factor stored ROW-major (Rt[i*n + j] = R[i, j]).      */
+
+AQR_API int64_t aqr_tile_rows(int64_t m);
+AQR_API int64_t aqr_num_tiles(int64_t m);
+
+/* z_i -= r * q_{i-1} (and x_i -= r * p_{i-1} when x/pprev given) where
+ * r = r_dev[0] (skipped when r_dev == NULL); then, if npart != NULL, the
+ * per-tile partials of (z.x, z.z, x.x) into npart[3 * ntiles]. */
+AQR_API aqr_status aqr_step_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
+                                    const double *pprev, const double *r_dev,
+                                    const double *xnorm, double *npart, const int32_t *status,
+                                    void *stream);
+/* tot[0..2] = fixed-order sums of npart (for the all-reduce) */
+AQR_API aqr_status aqr_step_norm_reduce(int64_t m, const double *npart, double *tot,
+                                const int32_t *status, void *stream);
+/* From tot: breakdown check (status), flag, R[i,i] = sqrt(t) into rii. */
+AQR_API aqr_status aqr_step_norm_finish(int64_t i, const double *tot, double *rii, int32_t *status,
+                                void *stream);
+/* q = z / rii ; p = x / rii when x != NULL */
+AQR_API aqr_status aqr_step_normalize(int64_t m, const double *z, const double *rii, double *q,
+                              const double *x, double *p, const int32_t *status, void *stream);
+/* The fused trailing pass of step i over columns [jbeg, jend) of W:
+ *   (q_i, p_i written when qout / pout given)
+ *   z_j -= r_{i-1,j} q_{i-1};  x_j -= r_{i-1,j} p_{i-1} (HP);
+ *   partial[(j - jbeg) * ntiles + tile] = sum over the tile of p_i . z_j
+ *   (p_i . z0_j for CGS). */
+AQR_API aqr_status aqr_step_trailing(int64_t m, int64_t i, int64_t jbeg, int64_t jend, double *W,
+                             int64_t ldw, double *X, int64_t ldx, const double *Z0,
+                             int64_t ldz0, const double *qprev, const double *pprev,
+                             const double *rprev, const double *psrc, const double *rii,
+                             double *pout, const double *zsrc, double *qout, double *partial,
+                             const int32_t *status, void *stream);
+/* out[c] = fixed-order sum over tiles of partial[c * ntiles + tile], c < ncols */
+AQR_API aqr_status aqr_step_rrow_reduce(int64_t m, int64_t ncols, const double *partial, double *out,
+                                const int32_t *status, void *stream);
+/* R (column-major, ldr) <- upper triangle of row-major Rt, zeros below */
+AQR_API aqr_status aqr_step_finalize_r(int64_t n, const double *Rt, double *R, int64_t ldr,
+                               void *stream);
+
+/* status block layout used by the step API: int32 [0] fail column (-1),
+ * [1] pad, then double fail value at byte 8, then int32 flags[n] at byte 16 */
+AQR_API uint64_t aqr_status_bytes(int64_t n);
+AQR_API aqr_status aqr_status_init(int32_t *status, int64_t n, void *stream);
+
+/* ---- instrumentation (bench.py) ------------------------------------------
+ * aqr_launch_count: number of kernels this library has launched so far in
+ * the process (monotonic; read before/after a timed region).
+ * aqr_trailing_timer_enable(1) makes aqr_gs_factor record a CUDA event pair
+ * around every fused trailing launch on the launching stream;
+ * aqr_trailing_timer_read returns the number of timed launches, their summed
+ * device time in ms and summed algorithmic bytes, then resets the timer
+ * (it synchronizes the recorded events). */
+AQR_API uint64_t aqr_launch_count(void);
+AQR_API aqr_status aqr_trailing_timer_enable(int32_t enable);
+AQR_API aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double *bytes);
+
+AQR_API const char *aqr_last_error(void);
+AQR_API int32_t aqr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AQR_B200_H */

@@ -29,8 +29,25 @@
 
 /* ---- L0 kernels: _kernels_impl.py ---------------------------------- */
 
+/* Tolerance calibration only: mode 1 swaps the
+ * sequential dot for a pairwise one, the perturbation a GPU tree reduction
+ * introduces.  Mode 0 (default) is the reference. */
+static int g_dot_mode = 0;
+void aqro_set_dot_mode(int mode) { g_dot_mode = mode; }
+
+static double pairwise_dot(int64_t m, const double *x, const double *y) {
+    if (m <= 8) {
+        double s = 0.0;
+        for (int64_t k = 0; k < m; ++k) s += x[k] * y[k];
+        return s;
+    }
+    const int64_t h = m / 2;
+    return pairwise_dot(h, x, y) + pairwise_dot(m - h, x + h, y + h);
+}
+
 /* _kernels_impl.py:17-21 */
 double aqro_seq_dot(int64_t m, const double *x, const double *y) {
+    if (g_dot_mode == 1) return pairwise_dot(m, x, y);
     double s = 0.0;
     for (int64_t k = 0; k < m; ++k) s += x[k] * y[k];
     return s;

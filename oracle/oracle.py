@@ -48,6 +48,8 @@ def lib():
                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                 _d, ctypes.c_int, _d, _i64, _i64, _d, _d, _d, _i32, _i64, _d,
             ]
+            L.aqro_set_dot_mode.restype = None
+            L.aqro_set_dot_mode.argtypes = [ctypes.c_int]
             L.aqro_householder_qr.restype = ctypes.c_int
             L.aqro_householder_qr.argtypes = [ctypes.c_int64, ctypes.c_int64, _d, _d]
             L.aqro_gemm_nn.restype = None
@@ -76,6 +78,22 @@ class OracleBreakdown(Exception):
 class OracleResult:
     def __init__(self, Q, R, flagged, mv_count):
         self.Q, self.R, self.flagged_columns, self.mv_count = Q, R, flagged, mv_count
+
+
+class pairwise_dots:
+    """Context manager: run the oracle with pairwise instead of sequential dots.
+
+    Used only to calibrate parity tolerances: the
+    spread between the two orders is the rounding noise any reordered
+    (e.g. GPU tree) reduction is entitled to.  Not thread-safe.
+    """
+
+    def __enter__(self):
+        lib().aqro_set_dot_mode(1)
+        return self
+
+    def __exit__(self, *exc):
+        lib().aqro_set_dot_mode(0)
 
 
 def seq_dot(x, y):

@@ -1,0 +1,104 @@
+"""Device-memory plumbing (torch is used for allocation and streams only).
+
+Column-major (Fortran) m x n device matrices are torch tensors of shape
+(m, n) with strides (1, ld): column j starts at data_ptr() + 8 * j * ld.
+"""
+
+import numpy as np
+
+from ._lib import ExtensionUnavailable
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def is_torch(x):
+    try:
+        import torch as t
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, t.Tensor)
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise ExtensionUnavailable("no CUDA device: the aqr B200 path has no CPU fallback")
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr():
+    return torch().cuda.current_stream().cuda_stream
+
+
+def empty_f(m, n, dev=None):
+    """Uninitialized column-major (m, n) fp64 device matrix (ld = m)."""
+    t = torch()
+    return t.empty((n, m), dtype=t.float64, device=dev or device()).t()
+
+
+def leading_dim(T):
+    """ld of a column-major 2-D tensor view, or None if not column-major."""
+    if T.dim() != 2:
+        return None
+    m, n = T.shape
+    s0, s1 = T.stride()
+    if (s0 == 1 or m <= 1) and (s1 >= max(m, 1) or n <= 1):
+        return max(s1, m, 1)
+    return None
+
+
+def to_device_f(a, dev=None):
+    """(device column-major fp64 tensor, ld) for a numpy array or tensor.
+
+    Never modifies ``a``; copies only when ``a`` is not already a column-major
+    fp64 tensor on the device.
+    """
+    t = torch()
+    dev = dev or device()
+    if is_torch(a):
+        T = a
+        if T.dtype != t.float64:
+            T = T.to(t.float64)
+        if T.device != dev:
+            T = T.to(dev, non_blocking=T.is_pinned())
+        ld = leading_dim(T)
+        if ld is None:
+            T = T.t().contiguous().t()
+            ld = leading_dim(T)
+        return T, ld
+    A = np.asfortranarray(a, dtype=np.float64)
+    T = t.from_numpy(A.T.copy(order="C") if not A.flags.f_contiguous else A.T).to(dev).t()
+    return T, max(A.shape[0], 1)
+
+
+class CudaArray:
+    """Zero-copy wrapper of a raw device pointer (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr, shape, strides_bytes, readonly=False):
+        self.__cuda_array_interface__ = {
+            "shape": tuple(int(s) for s in shape),
+            "typestr": "<f8",
+            "data": (int(ptr), readonly),
+            "version": 3,
+            "strides": tuple(int(s) for s in strides_bytes),
+            "stream": None,
+        }
+
+
+def wrap(ptr, m, k, ld):
+    """Torch view of a raw column-major device block (m x k, leading dim ld)."""
+    t = torch()
+    if k == 1:
+        arr = CudaArray(ptr, (m,), (8,))
+    else:
+        arr = CudaArray(ptr, (m, k), (8, 8 * ld))
+    return t.as_tensor(arr, device=device())

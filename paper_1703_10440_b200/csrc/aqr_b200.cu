@@ -1,0 +1,745 @@
+// aqr_b200.cu -- C ABI (include/aqr_b200.h) and the native step sequencer of
+// the A-orthogonal MGS factorization on B200 (sm_100a).
+//
+// The sequencer restates gram_schmidt._gs_factor
+// (/root/reference/pkg/src/aqr/gram_schmidt.py:126-179) as a one-pass-per-
+// step schedule: step i of the row form applies the deferred projection of
+// step i-1 to every trailing column and accumulates p_i . z_j in the same
+// HBM pass ("fused trailing pass").  The column form runs the
+// same kernels one column at a time, so both return bitwise-identical Q, R.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/aqr_b200.h"
+#include "aqr_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+aqr_status set_err(aqr_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+#define AQR_CUDA(call)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return set_err(AQR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define AQR_TRY(expr)                     \
+    do {                                  \
+        aqr_status s_ = (expr);           \
+        if (s_ != AQR_OK) return s_;      \
+    } while (0)
+
+std::atomic<uint64_t> g_launches{0};
+
+aqr_status launched(const char *what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(AQR_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return AQR_OK;
+}
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int elementwise_grid(int64_t m) {
+    int64_t g = (m + aqr::kBlock - 1) / aqr::kBlock;
+    return (int)std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 16);
+}
+
+// ---- operators -------------------------------------------------------------
+
+int auto_lanes(const aqr_op *op) {
+    if (op->spmv_lanes > 0) return op->spmv_lanes;
+    const double avg = op->m > 0 ? (double)op->nnz / (double)op->m : 1.0;
+    if (avg <= 1.5) return 1;
+    if (avg <= 4.0) return 4;
+    if (avg <= 8.0) return 8;
+    if (avg <= 16.0) return 16;
+    return 32;
+}
+
+aqr_status csr_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                     int64_t ldy, cudaStream_t s) {
+    const int L = auto_lanes(op);
+    const int64_t threads = op->m * L;
+    const int64_t grid = (threads + aqr::kBlock - 1) / aqr::kBlock;
+    if (grid == 0) return AQR_OK;
+    switch (L) {
+#define CASE(LL)                                                                                  \
+    case LL:                                                                                      \
+        aqr::csr_spmm_kernel<LL><<<(unsigned)grid, aqr::kBlock, 0, s>>>(op->m, k, op->indptr,     \
+                                                                        op->indices, op->data, X, \
+                                                                        ldx, Y, ldy);             \
+        break;
+        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
+#undef CASE
+        default:
+            return set_err(AQR_EARG, "spmv_lanes must be 1, 2, 4, 8, 16 or 32");
+    }
+    return launched("csr_spmm_kernel");
+}
+
+aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                       int64_t ldy, cudaStream_t s) {
+    const int64_t m = op->m;
+    if (m == 0) return AQR_OK;
+    if (k == 1) {
+        dim3 grid((unsigned)((m + aqr::kGemvBlock - 1) / aqr::kGemvBlock), 1);
+        aqr::dense_gemv_kernel<<<grid, aqr::kGemvBlock, 0, s>>>(m, op->A, op->lda, X, ldx, Y, ldy);
+        return launched("dense_gemv_kernel");
+    }
+    dim3 grid((unsigned)((m + aqr::kGemmBM - 1) / aqr::kGemmBM),
+              (unsigned)((k + aqr::kGemmBN - 1) / aqr::kGemmBN));
+    aqr::dense_gemm_kernel<<<grid, 256, 0, s>>>(m, k, op->A, op->lda, X, ldx, Y, ldy);
+    return launched("dense_gemm_kernel");
+}
+
+aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                    int64_t ldy, cudaStream_t s) {
+    if (!op) return set_err(AQR_EARG, "null operator");
+    switch (op->kind) {
+        case AQR_OP_DENSE:
+            if (!op->A || op->lda < op->m) return set_err(AQR_EARG, "dense operator: bad A/lda");
+            return dense_apply(op, k, X, ldx, Y, ldy, s);
+        case AQR_OP_CSR:
+            if (!op->indptr || (op->nnz && (!op->indices || !op->data)))
+                return set_err(AQR_EARG, "csr operator: null arrays");
+            return csr_apply(op, k, X, ldx, Y, ldy, s);
+        case AQR_OP_CALLBACK: {
+            aqr_apply_fn fn = (k > 1 && op->apply_block) ? op->apply_block : op->apply;
+            if (!fn) return set_err(AQR_EARG, "callback operator without apply");
+            if (k > 1 && fn == op->apply && !op->apply_block) {
+                for (int64_t c = 0; c < k; ++c)
+                    if (fn(op->ctx, 1, X + c * ldx, ldx, Y + c * ldy, ldy, s) != 0)
+                        return set_err(AQR_ECALLBACK, "operator apply callback failed");
+                return AQR_OK;
+            }
+            if (fn(op->ctx, k, X, ldx, Y, ldy, s) != 0)
+                return set_err(AQR_ECALLBACK, "operator apply callback failed");
+            return AQR_OK;
+        }
+        default:
+            return set_err(AQR_EARG, "unknown operator kind");
+    }
+}
+
+// ---- step launchers ----------------------------------------------------------
+
+aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
+                                  const double *pprev, const double *r, const double *xnorm,
+                                  double *npart, const int32_t *status, cudaStream_t s) {
+    aqr::ColArgs a;
+    a.m = m;
+    a.ntiles = (int32_t)aqr::num_tiles(m);
+    a.z = z;
+    a.qprev = qprev;
+    a.x = x;
+    a.pprev = pprev;
+    a.r = r;
+    a.xnorm = xnorm;
+    a.npart = npart;
+    a.status = status;
+    if (a.ntiles == 0) return AQR_OK;
+    if (aqr::rows_per_thread(m) == 8)
+        aqr::col_update_norm_kernel<8><<<a.ntiles, aqr::kBlock, 0, s>>>(a);
+    else
+        aqr::col_update_norm_kernel<1><<<a.ntiles, aqr::kBlock, 0, s>>>(a);
+    return launched("col_update_norm_kernel");
+}
+
+// Column-group size: enough CTAs to cover the chip (~4 CTAs per SM), at most
+// kMaxCpg columns per CTA (shared memory holds kWarps * cpg partials).
+constexpr int kMaxCpg = 256;
+int choose_cpg(int64_t ntiles, int64_t ncols) {
+    if (ncols <= 0) return 1;
+    const int64_t want_ctas = 148 * 4;
+    int64_t groups = std::max<int64_t>(1, (want_ctas + ntiles - 1) / ntiles);
+    groups = std::min<int64_t>(groups, ncols);
+    int64_t cpg = (ncols + groups - 1) / groups;
+    cpg = std::min<int64_t>(cpg, kMaxCpg);
+    return (int)std::max<int64_t>(cpg, 1);
+}
+
+// ---- trailing-kernel timer (bench.py's roofline leg) -------------------------
+struct TrailTimer {
+    std::mutex mu;
+    bool enabled = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;  // events in use (pairs)
+    double bytes = 0.0;
+    int64_t launches = 0;
+} g_timer;
+
+cudaEvent_t timer_event() {
+    if (g_timer.used == g_timer.pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        g_timer.pool.push_back(e);
+    }
+    return g_timer.pool[g_timer.used++];
+}
+
+// Algorithmic HBM bytes of one trailing launch: every trailing element read
+// once (and written once when the deferred update applies), the step's
+// vectors once.  Re-reads caused by column grouping are not counted.
+double trailing_bytes(const aqr::TrailArgs &a, bool hp, bool cgs) {
+    const double m = (double)a.m, t = (double)std::max(0, a.jend - a.jbeg);
+    const bool upd = a.qprev != nullptr;
+    double per_col = 8.0 + (upd ? 8.0 : 0.0) + ((hp && upd) ? 16.0 : 0.0) + (cgs ? 8.0 : 0.0);
+    double vec = 8.0 /* psrc */ + (upd ? 8.0 : 0.0) + ((hp && upd) ? 8.0 : 0.0) +
+                 (a.qout ? 16.0 : 0.0) + (a.pout ? 8.0 : 0.0);
+    return m * (t * per_col + vec);
+}
+
+aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStream_t s) {
+    aqr::TrailArgs a = a0;
+    const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
+    a.cpg = choose_cpg(a.ntiles, ncols);
+    const int64_t groups = ncols > 0 ? (ncols + a.cpg - 1) / a.cpg : 1;
+    dim3 grid((unsigned)a.ntiles, (unsigned)groups);
+    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
+    if (a.ntiles == 0) return AQR_OK;
+    const bool big = aqr::rows_per_thread(a.m) == 8;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_timer.mu);
+        if (g_timer.enabled) {
+            ev0 = timer_event();
+            ev1 = timer_event();
+            if (ev0 && ev1) {
+                cudaEventRecord(ev0, s);
+                g_timer.bytes += trailing_bytes(a, hp, cgs);
+                g_timer.launches += 1;
+            }
+        }
+    }
+#define LAUNCH(RPT, CU, HP, CGS) aqr::trailing_kernel<RPT, CU, HP, CGS><<<grid, aqr::kBlock, smem, s>>>(a)
+    if (big) {
+        if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
+        else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
+    } else {
+        if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
+        else    { if (cgs) LAUNCH(1, 4, false, true); else LAUNCH(1, 4, false, false); }
+    }
+#undef LAUNCH
+    if (ev0 && ev1) cudaEventRecord(ev1, s);
+    return launched("trailing_kernel");
+}
+
+aqr_status launch_rrow_reduce(int64_t m, int64_t ncols, const double *partial, double *out,
+                              const int32_t *status, cudaStream_t s) {
+    if (ncols <= 0) return AQR_OK;
+    aqr::rrow_reduce_kernel<<<(unsigned)ncols, aqr::kBlock, 0, s>>>(
+        partial, (int32_t)aqr::num_tiles(m), out, status);
+    return launched("rrow_reduce_kernel");
+}
+
+aqr_status launch_normalize(int64_t m, const double *z, const double *rii, double *q,
+                            const double *x, double *p, const int32_t *status, cudaStream_t s) {
+    aqr::normalize_kernel<<<elementwise_grid(m), aqr::kBlock, 0, s>>>(m, z, rii, q, x, p, status);
+    return launched("normalize_kernel");
+}
+
+// ---- workspace ---------------------------------------------------------------
+
+inline uint64_t al(uint64_t b) { return (b + 255) & ~uint64_t(255); }
+
+struct Layout {
+    uint64_t status, rt, partial, npart, xvec, pvec, pring, P, X, Z0, total;
+};
+
+Layout layout(int32_t family, int32_t variant, int32_t orientation, int64_t m, int64_t n) {
+    Layout L;
+    const uint64_t ntiles = (uint64_t)aqr::num_tiles(m);
+    const uint64_t mm = (uint64_t)m, nn = (uint64_t)n;
+    uint64_t off = 0;
+    auto take = [&](uint64_t bytes) {
+        uint64_t o = off;
+        off += al(bytes);
+        return o;
+    };
+    L.status = take(16 + 4 * nn);
+    L.rt = take(8 * nn * nn);
+    L.partial = take(8 * nn * std::max<uint64_t>(ntiles, 1));
+    L.npart = take(8 * 3 * std::max<uint64_t>(ntiles, 1));
+    L.xvec = variant != AQR_HP ? take(8 * mm) : ~0ull;
+    L.pvec = (variant == AQR_NAIVE && orientation == AQR_ROW) ? take(8 * mm) : ~0ull;
+    L.pring = (variant == AQR_HP && orientation == AQR_ROW) ? take(8 * 2 * mm) : ~0ull;
+    L.P = orientation == AQR_COL ? take(8 * mm * nn) : ~0ull;
+    L.X = variant == AQR_HP ? take(8 * mm * nn) : ~0ull;
+    L.Z0 = family == AQR_CGS ? take(8 * mm * nn) : ~0ull;
+    L.total = off;
+    return L;
+}
+
+template <typename T>
+T *at(void *base, uint64_t off) {
+    return off == ~0ull ? nullptr : reinterpret_cast<T *>(static_cast<char *>(base) + off);
+}
+
+// ---- the sequencer -------------------------------------------------------------
+
+struct Run {
+    aqr_factor_args *a;
+    cudaStream_t s;
+    bool hp, cgs, naive;
+    int64_t m, n;
+    double *W;  // == Q
+    int64_t ldw;
+    int32_t *status;
+    double *Rt, *partial, *npart, *xvec, *pvec, *pring, *P, *X, *Z0;
+    int64_t mv = 0;
+
+    double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
+    double *rt(int64_t i, int64_t j) const { return Rt + i * n + j; }
+
+    aqr_status mv1(const double *x, double *y) {
+        AQR_TRY(op_apply(a->op, 1, x, m, y, m, s));
+        ++mv;
+        return AQR_OK;
+    }
+
+    // z_j (and x_j) receive the deferred update with r_{j-1,j}; then x = A z
+    // (HA/naive) and the norm -> R[j,j], breakdown/flag (normalize(j) lines
+    // 148-160).  Returns the x column used.
+    aqr_status norm_step(int64_t j, const double *pprev_col, const double *&xcol) {
+        double *z = col(W, ldw, j);
+        const double *qprev = j > 0 ? col(W, ldw, j - 1) : nullptr;
+        const double *r = j > 0 ? rt(j - 1, j) : nullptr;
+        if (hp) {
+            double *x = col(X, m, j);
+            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, x, npart, status, s));
+            xcol = x;
+        } else {
+            if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, nullptr, status, s));
+            AQR_TRY(mv1(z, xvec));  // op.apply(Zw[:, j].copy()), line 151
+            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xvec, npart, status, s));
+            xcol = xvec;
+        }
+        const int32_t nt = (int32_t)aqr::num_tiles(m);
+        aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, s>>>(npart, nt, nullptr, j, rt(j, j), status);
+        return launched("norm_reduce_kernel");
+    }
+
+    aqr::TrailArgs trail(int64_t i, int64_t jbeg, int64_t jend) const {
+        aqr::TrailArgs t;
+        std::memset(&t, 0, sizeof t);
+        t.m = m;
+        t.ntiles = (int32_t)aqr::num_tiles(m);
+        t.jbeg = (int32_t)jbeg;
+        t.jend = (int32_t)jend;
+        t.W = W;
+        t.ldw = ldw;
+        t.X = X;
+        t.ldx = m;
+        t.Z0 = Z0;
+        t.ldz0 = m;
+        t.rprev = i > 0 ? Rt + (i - 1) * n : nullptr;
+        t.partial = partial;
+        t.status = status;
+        return t;
+    }
+
+    aqr_status row_form() {
+        for (int64_t i = 0; i < n; ++i) {
+            const double *pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
+            const double *xcol = nullptr;
+            AQR_TRY(norm_step(i, pprev, xcol));
+            aqr::TrailArgs t = trail(i, i + 1, n);
+            t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+            t.pprev = pprev;
+            if (naive) {
+                // q_i first, then p_i = A q_i (lines 161-163)
+                AQR_TRY(launch_normalize(m, col(W, ldw, i), rt(i, i), col(W, ldw, i), nullptr, nullptr, status, s));
+                AQR_TRY(mv1(col(W, ldw, i), pvec));
+                t.psrc = pvec;
+                t.rii = nullptr;
+            } else {
+                t.psrc = xcol;
+                t.rii = rt(i, i);
+                t.zsrc = col(W, ldw, i);
+                t.qout = col(W, ldw, i);
+                t.pout = hp ? pring + (i & 1) * m : nullptr;
+            }
+            AQR_TRY(launch_trailing(t, hp, cgs, s));
+            AQR_TRY(launch_rrow_reduce(m, n - 1 - i, partial, rt(i, i + 1), status, s));
+        }
+        return AQR_OK;
+    }
+
+    aqr_status col_form() {
+        for (int64_t j = 0; j < n; ++j) {
+            for (int64_t i = 0; i < j; ++i) {  // project(i, j), lines 169-170
+                aqr::TrailArgs t = trail(i, j, j + 1);
+                t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+                t.pprev = (hp && i > 0) ? col(P, m, i - 1) : nullptr;
+                t.psrc = col(P, m, i);
+                t.rii = nullptr;
+                AQR_TRY(launch_trailing(t, hp, cgs, s));
+                AQR_TRY(launch_rrow_reduce(m, 1, partial, rt(i, j), status, s));
+            }
+            const double *pprev = (hp && j > 0) ? col(P, m, j - 1) : nullptr;
+            const double *xcol = nullptr;
+            AQR_TRY(norm_step(j, pprev, xcol));  // normalize(j), line 171
+            if (naive) {
+                AQR_TRY(launch_normalize(m, col(W, ldw, j), rt(j, j), col(W, ldw, j), nullptr, nullptr, status, s));
+                AQR_TRY(mv1(col(W, ldw, j), col(P, m, j)));
+            } else {
+                AQR_TRY(launch_normalize(m, col(W, ldw, j), rt(j, j), col(W, ldw, j), xcol, col(P, m, j), status, s));
+            }
+        }
+        return AQR_OK;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char *aqr_last_error(void) { return g_err.c_str(); }
+uint64_t aqr_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+aqr_status aqr_trailing_timer_enable(int32_t enable) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    g_timer.enabled = enable != 0;
+    return AQR_OK;
+}
+
+aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double *bytes) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    double total = 0.0;
+    for (size_t k = 0; k + 1 < g_timer.used; k += 2) {
+        AQR_CUDA(cudaEventSynchronize(g_timer.pool[k + 1]));
+        float dt = 0.f;
+        AQR_CUDA(cudaEventElapsedTime(&dt, g_timer.pool[k], g_timer.pool[k + 1]));
+        total += dt;
+    }
+    if (launches) *launches = g_timer.launches;
+    if (ms) *ms = total;
+    if (bytes) *bytes = g_timer.bytes;
+    g_timer.used = 0;
+    g_timer.bytes = 0.0;
+    g_timer.launches = 0;
+    return AQR_OK;
+}
+int32_t aqr_abi_version(void) { return AQR_ABI_VERSION; }
+int64_t aqr_tile_rows(int64_t m) { return aqr::tile_rows(m); }
+int64_t aqr_num_tiles(int64_t m) { return aqr::num_tiles(m); }
+uint64_t aqr_status_bytes(int64_t n) { return 16 + 4 * (uint64_t)std::max<int64_t>(n, 0); }
+
+uint64_t aqr_workspace_bytes(int32_t family, int32_t variant, int32_t orientation, int64_t m,
+                             int64_t n) {
+    return layout(family, variant, orientation, m, n).total;
+}
+
+aqr_status aqr_status_init(int32_t *status, int64_t n, void *stream) {
+    const int64_t cnt = std::max<int64_t>(n, 1);
+    aqr::status_init_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, S(stream)>>>(status, n);
+    return launched("status_init_kernel");
+}
+
+aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
+    if (!a) return set_err(AQR_EARG, "null args");
+    a->fail_col = -1;
+    a->fail_val = 0.0;
+    a->mv_count = 0;
+    if (a->family < 0 || a->family > 1 || a->variant < 0 || a->variant > 2 || a->orientation < 0 ||
+        a->orientation > 1)
+        return set_err(AQR_EARG, "bad family/variant/orientation");
+    const int64_t m = a->m, n = a->n;
+    if (n < 1 || m < n) return set_err(AQR_EDIM, "need m >= n >= 1");
+    if (!a->op || a->op->m != m) return set_err(AQR_EDIM, "operator dimension does not match Z");
+    if (n > (int64_t)INT32_MAX || m > ((int64_t)1 << 40)) return set_err(AQR_EARG, "size out of range");
+    if (!a->Z || !a->Q || !a->R || a->ldz < m || a->ldq < m || a->ldr < n)
+        return set_err(AQR_EARG, "bad Z/Q/R pointer or leading dimension");
+    const Layout L = layout(a->family, a->variant, a->orientation, m, n);
+    if (!a->workspace || a->workspace_bytes < L.total)
+        return set_err(AQR_ENOMEM, "workspace smaller than aqr_workspace_bytes()");
+
+    Run r;
+    r.a = a;
+    r.s = S(stream);
+    r.hp = a->variant == AQR_HP;
+    r.naive = a->variant == AQR_NAIVE;
+    r.cgs = a->family == AQR_CGS;
+    r.m = m;
+    r.n = n;
+    r.W = a->Q;
+    r.ldw = a->ldq;
+    void *ws = a->workspace;
+    r.status = at<int32_t>(ws, L.status);
+    r.Rt = at<double>(ws, L.rt);
+    r.partial = at<double>(ws, L.partial);
+    r.npart = at<double>(ws, L.npart);
+    r.xvec = at<double>(ws, L.xvec);
+    r.pvec = at<double>(ws, L.pvec);
+    r.pring = at<double>(ws, L.pring);
+    r.P = at<double>(ws, L.P);
+    r.X = at<double>(ws, L.X);
+    r.Z0 = at<double>(ws, L.Z0);
+    cudaStream_t s = r.s;
+
+    if (a->Z != a->Q)  // Zw = Z.copy(order="F"), line 131
+        AQR_CUDA(cudaMemcpy2DAsync(a->Q, a->ldq * 8, a->Z, a->ldz * 8, m * 8, n, cudaMemcpyDeviceToDevice, s));
+    AQR_TRY(aqr_status_init(r.status, n, stream));
+    AQR_CUDA(cudaMemsetAsync(r.Rt, 0, 8 * (size_t)n * n, s));
+    if (r.cgs)  // Z0, line 132
+        AQR_CUDA(cudaMemcpy2DAsync(r.Z0, m * 8, a->Q, a->ldq * 8, m * 8, n, cudaMemcpyDeviceToDevice, s));
+    if (r.hp) {  // X = op.apply_block(Zw)
+        AQR_TRY(op_apply(a->op, n, a->Q, a->ldq, r.X, m, s));
+        r.mv += n;
+    }
+    AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
+    aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, r.Rt, a->R, a->ldr);
+    AQR_TRY(launched("finalize_r_kernel"));
+    std::vector<int32_t> st((16 + 4 * n) / 4);
+    AQR_CUDA(cudaMemcpyAsync(st.data(), r.status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
+    AQR_CUDA(cudaStreamSynchronize(s));
+    a->mv_count = r.mv;
+    if (a->flagged_host) std::memcpy(a->flagged_host, st.data() + 4, 4 * n);
+    if (st[0] >= 0) {
+        a->fail_col = st[0];
+        std::memcpy(&a->fail_val, st.data() + 2, 8);
+        return set_err(AQR_EBREAKDOWN, "breakdown at column " + std::to_string(st[0]));
+    }
+    return AQR_OK;
+}
+
+aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientation, int64_t m,
+                              int64_t n, const double *Z_host, double *Q_host, double *R_host,
+                              int32_t op_kind, const double *A_host, const int64_t *indptr_host,
+                              const int64_t *indices_host, const double *data_host, int64_t nnz,
+                              int64_t *fail_col, double *fail_val, int32_t *flagged_host,
+                              int64_t *mv_count) {
+    if (n < 1 || m < n) return set_err(AQR_EDIM, "need m >= n >= 1");
+    if (op_kind == AQR_OP_CSR && nnz >= ((int64_t)1 << 31))
+        return set_err(AQR_EARG, "nnz >= 2^31 does not fit the int32 CSR layout");
+    cudaStream_t s;
+    AQR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    std::vector<void *> bufs;
+    auto dalloc = [&](size_t bytes) -> void * {
+        void *p = nullptr;
+        if (cudaMallocAsync(&p, std::max<size_t>(bytes, 256), s) != cudaSuccess) return nullptr;
+        bufs.push_back(p);
+        return p;
+    };
+    auto cleanup = [&]() {
+        for (void *p : bufs) cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+    };
+    aqr_op op;
+    std::memset(&op, 0, sizeof op);
+    op.kind = op_kind;
+    op.m = m;
+    aqr_status st = AQR_OK;
+    double *Q = (double *)dalloc(8 * (size_t)m * n);
+    double *R = (double *)dalloc(8 * (size_t)n * n);
+    const uint64_t wsb = aqr_workspace_bytes(family, variant, orientation, m, n);
+    void *ws = dalloc(wsb);
+    std::vector<int32_t> ip32, ix32;
+    if (!Q || !R || !ws) st = set_err(AQR_ENOMEM, "device allocation failed");
+    if (st == AQR_OK && op_kind == AQR_OP_DENSE) {
+        double *A = (double *)dalloc(8 * (size_t)m * m);
+        if (!A) st = set_err(AQR_ENOMEM, "device allocation failed");
+        else if (cudaMemcpyAsync(A, A_host, 8 * (size_t)m * m, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            st = set_err(AQR_ECUDA, "H2D A");
+        op.A = A;
+        op.lda = m;
+    } else if (st == AQR_OK && op_kind == AQR_OP_CSR) {
+        ip32.resize(m + 1);
+        ix32.resize(nnz);
+        for (int64_t i = 0; i <= m; ++i) ip32[i] = (int32_t)indptr_host[i];
+        for (int64_t k = 0; k < nnz; ++k) ix32[k] = (int32_t)indices_host[k];
+        int32_t *ip = (int32_t *)dalloc(4 * (size_t)(m + 1));
+        int32_t *ix = (int32_t *)dalloc(4 * (size_t)nnz);
+        double *dv = (double *)dalloc(8 * (size_t)nnz);
+        if (!ip || !ix || !dv) st = set_err(AQR_ENOMEM, "device allocation failed");
+        else if (cudaMemcpyAsync(ip, ip32.data(), 4 * (m + 1), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                 cudaMemcpyAsync(ix, ix32.data(), 4 * nnz, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+                 cudaMemcpyAsync(dv, data_host, 8 * nnz, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            st = set_err(AQR_ECUDA, "H2D CSR");
+        op.indptr = ip;
+        op.indices = ix;
+        op.data = dv;
+        op.nnz = nnz;
+    } else if (st == AQR_OK) {
+        st = set_err(AQR_EARG, "host entry supports dense and CSR operators");
+    }
+    if (st == AQR_OK && cudaMemcpyAsync(Q, Z_host, 8 * (size_t)m * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        st = set_err(AQR_ECUDA, "H2D Z");
+    aqr_factor_args a;
+    std::memset(&a, 0, sizeof a);
+    if (st == AQR_OK) {
+        a.family = family;
+        a.variant = variant;
+        a.orientation = orientation;
+        a.m = m;
+        a.n = n;
+        a.Z = Q;
+        a.ldz = m;
+        a.Q = Q;
+        a.ldq = m;
+        a.R = R;
+        a.ldr = n;
+        a.op = &op;
+        a.workspace = ws;
+        a.workspace_bytes = wsb;
+        a.flagged_host = flagged_host;
+        st = aqr_gs_factor(&a, s);
+        if (fail_col) *fail_col = a.fail_col;
+        if (fail_val) *fail_val = a.fail_val;
+        if (mv_count) *mv_count = a.mv_count;
+    }
+    if (st == AQR_OK) {
+        if (cudaMemcpyAsync(Q_host, Q, 8 * (size_t)m * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(R_host, R, 8 * (size_t)n * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            st = set_err(AQR_ECUDA, "D2H Q/R");
+    }
+    cleanup();
+    return st;
+}
+
+aqr_status aqr_op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                        int64_t ldy, void *stream) {
+    if (!op || k < 0 || ldx < op->m || ldy < op->m) return set_err(AQR_EARG, "bad apply arguments");
+    if (k == 0) return AQR_OK;
+    return op_apply(op, k, X, ldx, Y, ldy, S(stream));
+}
+
+aqr_status aqr_dot(int64_t m, const double *x, const double *y, double *out, void *stream) {
+    const int64_t nt = aqr::num_tiles(m);
+    if (nt == 0) return set_err(AQR_EARG, "empty vector");
+    double *part = nullptr;
+    AQR_CUDA(cudaMallocAsync(&part, 8 * nt, S(stream)));
+    aqr::dot_partial_kernel<<<(unsigned)nt, aqr::kBlock, 0, S(stream)>>>(m, aqr::rows_per_thread(m), x, y, part);
+    aqr_status st = launched("dot_partial_kernel");
+    if (st == AQR_OK) st = launch_rrow_reduce(m, 1, part, out, nullptr, S(stream));
+    cudaFreeAsync(part, S(stream));
+    return st;
+}
+
+aqr_status aqr_sub_scaled(int64_t m, double *z, const double *a_dev, const double *q, void *stream) {
+    aqr::sub_scaled_kernel<<<elementwise_grid(m), aqr::kBlock, 0, S(stream)>>>(m, z, a_dev, q);
+    return launched("sub_scaled_kernel");
+}
+
+aqr_status aqr_div_scalar(int64_t m, const double *x, const double *r_dev, double *out, void *stream) {
+    aqr::div_scalar_kernel<<<elementwise_grid(m), aqr::kBlock, 0, S(stream)>>>(m, x, r_dev, out);
+    return launched("div_scalar_kernel");
+}
+
+aqr_status aqr_matvec(int64_t m, const double *A, int64_t lda, const double *x, double *y, void *stream) {
+    aqr_op op;
+    std::memset(&op, 0, sizeof op);
+    op.kind = AQR_OP_DENSE;
+    op.m = m;
+    op.A = A;
+    op.lda = lda;
+    return aqr_op_apply(&op, 1, x, m, y, m, stream);
+}
+
+aqr_status aqr_apply_block_dense(int64_t m, int64_t k, const double *A, int64_t lda, const double *X,
+                                 int64_t ldx, double *Y, int64_t ldy, void *stream) {
+    aqr_op op;
+    std::memset(&op, 0, sizeof op);
+    op.kind = AQR_OP_DENSE;
+    op.m = m;
+    op.A = A;
+    op.lda = lda;
+    return aqr_op_apply(&op, k, X, ldx, Y, ldy, stream);
+}
+
+aqr_status aqr_csr_matvec(int64_t m, const int32_t *indptr, const int32_t *indices, const double *data,
+                          const double *x, double *y, void *stream) {
+    aqr_op op;
+    std::memset(&op, 0, sizeof op);
+    op.kind = AQR_OP_CSR;
+    op.m = m;
+    op.indptr = indptr;
+    op.indices = indices;
+    op.data = data;
+    op.spmv_lanes = 8;  // explicit: no nnz needed to pick the lane count
+    return aqr_op_apply(&op, 1, x, m, y, m, stream);
+}
+
+aqr_status aqr_step_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
+                                    const double *pprev, const double *r_dev, const double *xnorm,
+                                    double *npart, const int32_t *status, void *stream) {
+    return launch_col_update_norm(m, z, qprev, x, pprev, r_dev, xnorm, npart, status, S(stream));
+}
+
+aqr_status aqr_step_norm_reduce(int64_t m, const double *npart, double *tot, const int32_t *status,
+                                void *stream) {
+    aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, S(stream)>>>(npart, (int32_t)aqr::num_tiles(m), tot, 0,
+                                                            nullptr, const_cast<int32_t *>(status));
+    return launched("norm_reduce_kernel");
+}
+
+aqr_status aqr_step_norm_finish(int64_t i, const double *tot, double *rii, int32_t *status, void *stream) {
+    aqr::norm_finish_kernel<<<1, 1, 0, S(stream)>>>(i, tot, rii, status);
+    return launched("norm_finish_kernel");
+}
+
+aqr_status aqr_step_normalize(int64_t m, const double *z, const double *rii, double *q, const double *x,
+                              double *p, const int32_t *status, void *stream) {
+    return launch_normalize(m, z, rii, q, x, p, status, S(stream));
+}
+
+aqr_status aqr_step_trailing(int64_t m, int64_t i, int64_t jbeg, int64_t jend, double *W, int64_t ldw,
+                             double *X, int64_t ldx, const double *Z0, int64_t ldz0, const double *qprev,
+                             const double *pprev, const double *rprev, const double *psrc,
+                             const double *rii, double *pout, const double *zsrc, double *qout,
+                             double *partial, const int32_t *status, void *stream) {
+    (void)i;
+    aqr::TrailArgs t;
+    std::memset(&t, 0, sizeof t);
+    t.m = m;
+    t.ntiles = (int32_t)aqr::num_tiles(m);
+    t.jbeg = (int32_t)jbeg;
+    t.jend = (int32_t)jend;
+    t.W = W;
+    t.ldw = ldw;
+    t.X = X;
+    t.ldx = ldx;
+    t.Z0 = Z0;
+    t.ldz0 = ldz0;
+    t.qprev = qprev;
+    t.pprev = pprev;
+    t.rprev = rprev;
+    t.psrc = psrc;
+    t.rii = rii;
+    t.pout = pout;
+    t.zsrc = zsrc;
+    t.qout = qout;
+    t.partial = partial;
+    t.status = status;
+    if (qprev && !rprev) return set_err(AQR_EARG, "qprev without rprev");
+    if (X == nullptr && pprev != nullptr) return set_err(AQR_EARG, "pprev without X");
+    return launch_trailing(t, X != nullptr, Z0 != nullptr, S(stream));
+}
+
+aqr_status aqr_step_rrow_reduce(int64_t m, int64_t ncols, const double *partial, double *out,
+                                const int32_t *status, void *stream) {
+    return launch_rrow_reduce(m, ncols, partial, out, status, S(stream));
+}
+
+aqr_status aqr_step_finalize_r(int64_t n, const double *Rt, double *R, int64_t ldr, void *stream) {
+    aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, S(stream)>>>(n, Rt, R, ldr);
+    return launched("finalize_r_kernel");
+}
+
+}  // extern "C"

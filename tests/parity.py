@@ -1,0 +1,44 @@
+"""Parity metrics and calibrated tolerances (test infrastructure).
+
+The B200 kernels reproduce every elementwise operation and every operator
+product of the reference bit for bit; only the dot-product reductions are
+reordered (deterministic tree instead of a sequential chain).  The tolerance
+for a case is therefore calibrated on the case itself: TOL_FACTOR times the
+spread between the oracle with sequential dots (the reference) and the
+oracle with pairwise dots (oracle.pairwise_dots), floored at FLOOR.
+"""
+
+import numpy as np
+
+from oracle import oracle as O
+
+TOL_FACTOR = 100.0
+FLOOR = 1e-13
+Q_COLUMN_FLOOR = 1e-3
+
+
+def _np(a):
+    return np.asarray(a.cpu() if hasattr(a, "cpu") else a)
+
+
+def factor_errors(Q, R, Qref, Rref):
+    """(Q error with column-norm floor, max|dR| / max|R|)."""
+    Q, R, Qref, Rref = map(_np, (Q, R, Qref, Rref))
+    colmax = np.abs(Qref).max(axis=0, keepdims=True)
+    den = np.maximum(np.abs(Qref), Q_COLUMN_FLOOR * colmax)
+    den = np.where(den > 0, den, 1.0)
+    eq = float(np.max(np.abs(Q - Qref) / den))
+    er = float(np.max(np.abs(R - Rref)) / max(float(np.max(np.abs(Rref))), 1e-300))
+    return eq, er
+
+
+def spread(Z, spec, method):
+    seq = O.gs_factor(Z, spec, method)
+    with O.pairwise_dots():
+        pw = O.gs_factor(Z, spec, method)
+    return factor_errors(pw.Q, pw.R, seq.Q, seq.R)
+
+
+def tolerance(Z, spec, method):
+    sq, sr = spread(Z, spec, method)
+    return max(TOL_FACTOR * sq, FLOOR), max(TOL_FACTOR * sr, FLOOR)
