@@ -218,6 +218,9 @@ AQR_API aqr_status aqr_status_init(int32_t *status, int64_t n, void *stream);
 AQR_API uint64_t aqr_launch_count(void);
 AQR_API aqr_status aqr_trailing_timer_enable(int32_t enable);
 AQR_API aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double *bytes);
+/* Same for any timed kernel slot (0 trailing, 1 fused SpMV step, 2 column
+ * update + norm), without resetting; enabling the timer resets it. */
+AQR_API aqr_status aqr_kernel_timer_read(int32_t slot, int64_t *launches, double *ms, double *bytes);
 
 AQR_API const char *aqr_last_error(void);
 AQR_API int32_t aqr_abi_version(void);

@@ -86,6 +86,8 @@ SIGNATURES = {
     "aqr_trailing_timer_enable": (c_i32, [c_i32]),
     "aqr_trailing_timer_read": (c_i32, [ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl),
                                         ctypes.POINTER(c_dbl)]),
+    "aqr_kernel_timer_read": (c_i32, [c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl),
+                                      ctypes.POINTER(c_dbl)]),
     "aqr_last_error": (ctypes.c_char_p, []),
     "aqr_abi_version": (c_i32, []),
 }

@@ -5,15 +5,21 @@
 // (/root/reference/pkg/src/aqr/gram_schmidt.py:126-179) as a one-pass-per-
 // step schedule: step i of the row form applies the deferred projection of
 // step i-1 to every trailing column and accumulates p_i . z_j in the same
-// HBM pass ("fused trailing pass").  The column form runs the
-// same kernels one column at a time, so both return bitwise-identical Q, R.
+// HBM pass ("fused trailing pass").  With a native CSR operator a
+// HA/naive step is two launches: the fused SpMV step (z update + x = A z +
+// norm + r_ii) and the fused trailing pass (+ the r row); both finish their
+// reductions in the last CTA, so there are no separate reduction launches.
+// The column form runs the same kernels one column at a time, so both
+// orientations return bitwise-identical Q, R.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <atomic>
-#include <mutex>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -23,6 +29,7 @@
 namespace {
 
 thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
 
 aqr_status set_err(aqr_status s, const std::string &msg) {
     g_err = msg;
@@ -36,13 +43,11 @@ aqr_status set_err(aqr_status s, const std::string &msg) {
             return set_err(AQR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-#define AQR_TRY(expr)                     \
-    do {                                  \
-        aqr_status s_ = (expr);           \
-        if (s_ != AQR_OK) return s_;      \
+#define AQR_TRY(expr)                \
+    do {                             \
+        aqr_status s_ = (expr);      \
+        if (s_ != AQR_OK) return s_; \
     } while (0)
-
-std::atomic<uint64_t> g_launches{0};
 
 aqr_status launched(const char *what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -58,37 +63,131 @@ int elementwise_grid(int64_t m) {
     return (int)std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 16);
 }
 
-// ---- operators -------------------------------------------------------------
-
-int auto_lanes(const aqr_op *op) {
-    if (op->spmv_lanes > 0) return op->spmv_lanes;
-    const double avg = op->m > 0 ? (double)op->nnz / (double)op->m : 1.0;
-    if (avg <= 1.5) return 1;
-    if (avg <= 4.0) return 4;
-    if (avg <= 8.0) return 8;
-    if (avg <= 16.0) return 16;
-    return 32;
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cached[dev] == 0) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
 }
 
-aqr_status csr_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
-                     int64_t ldy, cudaStream_t s) {
-    const int L = auto_lanes(op);
-    const int64_t threads = op->m * L;
-    const int64_t grid = (threads + aqr::kBlock - 1) / aqr::kBlock;
-    if (grid == 0) return AQR_OK;
-    switch (L) {
-#define CASE(LL)                                                                                  \
-    case LL:                                                                                      \
-        aqr::csr_spmm_kernel<LL><<<(unsigned)grid, aqr::kBlock, 0, s>>>(op->m, k, op->indptr,     \
-                                                                        op->indices, op->data, X, \
-                                                                        ldx, Y, ldy);             \
-        break;
-        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32)
-#undef CASE
-        default:
-            return set_err(AQR_EARG, "spmv_lanes must be 1, 2, 4, 8, 16 or 32");
+// Opt a kernel into > 48 KB of dynamic shared memory (once per device and
+// kernel: the attribute is sticky, and setting it on every launch costs
+// host time on the latency-bound small steps).
+template <typename K>
+aqr_status ensure_smem(K kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return AQR_OK;
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void *, int>, size_t>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void *key = reinterpret_cast<const void *>(kernel);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &e : done)
+        if (e.first.first == key && e.first.second == dev && e.second >= bytes) return AQR_OK;
+    AQR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done.push_back({{key, dev}, bytes});
+    return AQR_OK;
+}
+
+// ---- kernel timer (bench.py's roofline leg) ---------------------------------
+// Slot 0: fused trailing pass; slot 1: fused SpMV step; slot 2: column
+// update + norm.  When enabled, a CUDA event pair is recorded around every
+// launch of those kernels on the launching stream.
+struct KernelTimer {
+    struct Rec {
+        int slot;
+        cudaEvent_t e0, e1;
+        double bytes;
+    };
+    std::mutex mu;
+    bool enabled = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<Rec> recs;
+} g_timer;
+
+cudaEvent_t timer_event() {
+    if (g_timer.used == g_timer.pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        g_timer.pool.push_back(e);
     }
-    return launched("csr_spmm_kernel");
+    return g_timer.pool[g_timer.used++];
+}
+
+// Returns the record index, or -1 when the timer is off.
+long timer_begin(int slot, double bytes, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    if (!g_timer.enabled) return -1;
+    cudaEvent_t e0 = timer_event(), e1 = timer_event();
+    if (!e0 || !e1) return -1;
+    cudaEventRecord(e0, s);
+    g_timer.recs.push_back({slot, e0, e1, bytes});
+    return (long)g_timer.recs.size() - 1;
+}
+
+void timer_end(long idx, cudaStream_t s) {
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    cudaEventRecord(g_timer.recs[(size_t)idx].e1, s);
+}
+
+// Experiment knob (read once): AQR_TRAIL_VARIANT = 0 TMA + L2 evict-first
+// hint (default), 1 TMA without hint, 2 generic LDG kernel.
+int trail_variant() {
+    static const int v = [] {
+        const char *e = std::getenv("AQR_TRAIL_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// ---- operators ---------------------------------------------------------------
+
+aqr::NormOut no_norm() {
+    aqr::NormOut o;
+    std::memset(&o, 0, sizeof o);
+    return o;
+}
+
+aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                      int64_t ldy, const double *qprev, const double *r, double *znew,
+                      const aqr::NormOut &out, cudaStream_t s) {
+    aqr::CsrArgs a;
+    a.m = op->m;
+    a.k = k;
+    a.indptr = op->indptr;
+    a.indices = op->indices;
+    a.data = op->data;
+    a.X = X;
+    a.ldx = ldx;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.qprev = qprev;
+    a.r = r;
+    a.znew = znew;
+    a.out = out;
+    if (op->m == 0) return AQR_OK;
+    // 256-row blocks (== the canonical norm tiles when fused), grid-stride
+    // over a persistent grid: one completion ticket per CTA.
+    const int64_t nblocks = (op->m + aqr::kBlock - 1) / aqr::kBlock;
+    const int64_t grid = std::min<int64_t>(nblocks, (int64_t)sm_count() * 8);
+    if (out.npart != nullptr) {
+        const int64_t nt = aqr::norm_tiles(op->m);
+        const long tix = timer_begin(1, (double)op->m * 40.0 + (double)op->nnz * 12.0, s);
+        aqr::csr_step_kernel<<<(unsigned)std::min<int64_t>(nt, (int64_t)sm_count() * 8), aqr::kBlock, 0,
+                                  s>>>(a);
+        timer_end(tix, s);
+        return launched("csr_step_kernel");
+    }
+    aqr::csr_row_kernel<<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    return launched("csr_row_kernel");
 }
 
 aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
@@ -116,11 +215,11 @@ aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, d
         case AQR_OP_CSR:
             if (!op->indptr || (op->nnz && (!op->indices || !op->data)))
                 return set_err(AQR_EARG, "csr operator: null arrays");
-            return csr_apply(op, k, X, ldx, Y, ldy, s);
+            return launch_csr(op, k, X, ldx, Y, ldy, nullptr, nullptr, nullptr, no_norm(), s);
         case AQR_OP_CALLBACK: {
             aqr_apply_fn fn = (k > 1 && op->apply_block) ? op->apply_block : op->apply;
             if (!fn) return set_err(AQR_EARG, "callback operator without apply");
-            if (k > 1 && fn == op->apply && !op->apply_block) {
+            if (k > 1 && !op->apply_block) {
                 for (int64_t c = 0; c < k; ++c)
                     if (fn(op->ctx, 1, X + c * ldx, ldx, Y + c * ldy, ldy, s) != 0)
                         return set_err(AQR_ECALLBACK, "operator apply callback failed");
@@ -135,60 +234,29 @@ aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, d
     }
 }
 
-// ---- step launchers ----------------------------------------------------------
+// ---- step launchers ------------------------------------------------------------
 
 aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
                                   const double *pprev, const double *r, const double *xnorm,
-                                  double *npart, const int32_t *status, cudaStream_t s) {
+                                  const aqr::NormOut &out, cudaStream_t s) {
     aqr::ColArgs a;
     a.m = m;
-    a.ntiles = (int32_t)aqr::num_tiles(m);
     a.z = z;
     a.qprev = qprev;
     a.x = x;
     a.pprev = pprev;
     a.r = r;
     a.xnorm = xnorm;
-    a.npart = npart;
-    a.status = status;
-    if (a.ntiles == 0) return AQR_OK;
-    if (aqr::rows_per_thread(m) == 8)
-        aqr::col_update_norm_kernel<8><<<a.ntiles, aqr::kBlock, 0, s>>>(a);
-    else
-        aqr::col_update_norm_kernel<1><<<a.ntiles, aqr::kBlock, 0, s>>>(a);
+    a.out = out;
+    a.out.ntiles = (int32_t)aqr::norm_tiles(m);
+    const int64_t nt = aqr::norm_tiles(m);
+    if (nt == 0) return AQR_OK;
+    const int64_t grid = std::min<int64_t>(nt, (int64_t)sm_count() * 8);
+    const long tix = timer_begin(2, (double)m * (8.0 + (r ? 16.0 : 0.0) + (x ? (r ? 24.0 : 8.0) : 0.0) +
+                                                 (xnorm ? 8.0 : 0.0)), s);
+    aqr::col_update_norm_kernel<<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    timer_end(tix, s);
     return launched("col_update_norm_kernel");
-}
-
-// Column-group size: enough CTAs to cover the chip (~4 CTAs per SM), at most
-// kMaxCpg columns per CTA (shared memory holds kWarps * cpg partials).
-constexpr int kMaxCpg = 256;
-int choose_cpg(int64_t ntiles, int64_t ncols) {
-    if (ncols <= 0) return 1;
-    const int64_t want_ctas = 148 * 4;
-    int64_t groups = std::max<int64_t>(1, (want_ctas + ntiles - 1) / ntiles);
-    groups = std::min<int64_t>(groups, ncols);
-    int64_t cpg = (ncols + groups - 1) / groups;
-    cpg = std::min<int64_t>(cpg, kMaxCpg);
-    return (int)std::max<int64_t>(cpg, 1);
-}
-
-// ---- trailing-kernel timer (bench.py's roofline leg) -------------------------
-struct TrailTimer {
-    std::mutex mu;
-    bool enabled = false;
-    std::vector<cudaEvent_t> pool;
-    size_t used = 0;  // events in use (pairs)
-    double bytes = 0.0;
-    int64_t launches = 0;
-} g_timer;
-
-cudaEvent_t timer_event() {
-    if (g_timer.used == g_timer.pool.size()) {
-        cudaEvent_t e;
-        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
-        g_timer.pool.push_back(e);
-    }
-    return g_timer.pool[g_timer.used++];
 }
 
 // Algorithmic HBM bytes of one trailing launch: every trailing element read
@@ -203,46 +271,89 @@ double trailing_bytes(const aqr::TrailArgs &a, bool hp, bool cgs) {
     return m * (t * per_col + vec);
 }
 
+// Generic kernel: column groups so that ~4 CTAs per SM are in flight.
+constexpr int kMaxCpg = 256;
+int choose_cpg_generic(int64_t ntiles, int64_t ncols) {
+    if (ncols <= 0) return 1;
+    const int64_t want_ctas = (int64_t)sm_count() * 4;
+    int64_t groups = std::max<int64_t>(1, (want_ctas + ntiles - 1) / ntiles);
+    groups = std::min<int64_t>(groups, ncols);
+    int64_t cpg = (ncols + groups - 1) / groups;
+    cpg = std::min<int64_t>(cpg, kMaxCpg);
+    return (int)std::max<int64_t>(cpg, 1);
+}
+
+aqr_status launch_rrow_reduce(int64_t m, int64_t ncols, const double *partial, double *out,
+                              const int32_t *status, cudaStream_t s);
+
 aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStream_t s) {
     aqr::TrailArgs a = a0;
     const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
-    a.cpg = choose_cpg(a.ntiles, ncols);
-    const int64_t groups = ncols > 0 ? (ncols + a.cpg - 1) / a.cpg : 1;
-    dim3 grid((unsigned)a.ntiles, (unsigned)groups);
-    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
     if (a.ntiles == 0) return AQR_OK;
     const bool big = aqr::rows_per_thread(a.m) == 8;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    {
-        std::lock_guard<std::mutex> lk(g_timer.mu);
-        if (g_timer.enabled) {
-            ev0 = timer_event();
-            ev1 = timer_event();
-            if (ev0 && ev1) {
-                cudaEventRecord(ev0, s);
-                g_timer.bytes += trailing_bytes(a, hp, cgs);
-                g_timer.launches += 1;
-            }
-        }
-    }
-#define LAUNCH(RPT, CU, HP, CGS) aqr::trailing_kernel<RPT, CU, HP, CGS><<<grid, aqr::kBlock, smem, s>>>(a)
-    if (big) {
-        if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
-        else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
+    const bool aligned = (a.ldw % 2 == 0) && (!hp || a.ldx % 2 == 0) && (!cgs || a.ldz0 % 2 == 0) &&
+                         ((uintptr_t)a.W % 16 == 0) && (!hp || (uintptr_t)a.X % 16 == 0) &&
+                         (!cgs || (uintptr_t)a.Z0 % 16 == 0);
+    const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && trail_variant() != 2;
+    a.cpg = tma ? (int32_t)std::max<int64_t>(ncols, 1) : choose_cpg_generic(a.ntiles, ncols);
+    a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
+
+    const long tix = timer_begin(0, trailing_bytes(a, hp, cgs), s);
+    if (tma) {
+        const int64_t units = (int64_t)a.ntiles * std::max<int64_t>(ncols, 1);
+#define TMA_LAUNCH(HP, CGS)                                                                      \
+    do {                                                                                         \
+        constexpr size_t smem = aqr::TmaCfg<HP, CGS>::kSmem;                                     \
+        AQR_TRY(ensure_smem(aqr::trailing_tma_kernel<HP, CGS, true>, smem));                     \
+        AQR_TRY(ensure_smem(aqr::trailing_tma_kernel<HP, CGS, false>, smem));                    \
+        /* all CTAs must be co-resident: the last ones wait for the grid */                     \
+        static int occ[64] = {0};                                                                \
+        int dev_ = 0;                                                                            \
+        cudaGetDevice(&dev_);                                                                    \
+        if (occ[dev_ & 63] == 0) {                                                               \
+            int o_ = 0;                                                                          \
+            AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                              \
+                &o_, aqr::trailing_tma_kernel<HP, CGS, true>, aqr::kTmaThreads, smem));          \
+            occ[dev_ & 63] = std::max(1, std::min(o_, 2));                                       \
+        }                                                                                        \
+        const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sm_count() * occ[dev_ & 63]); \
+        if (trail_variant() == 1)                                                                \
+            aqr::trailing_tma_kernel<HP, CGS, false><<<grid, aqr::kTmaThreads, smem, s>>>(a);    \
+        else                                                                                     \
+            aqr::trailing_tma_kernel<HP, CGS, true><<<grid, aqr::kTmaThreads, smem, s>>>(a);     \
+    } while (0)
+        if (hp) { if (cgs) TMA_LAUNCH(true, true); else TMA_LAUNCH(true, false); }
+        else    { if (cgs) TMA_LAUNCH(false, true); else TMA_LAUNCH(false, false); }
+#undef TMA_LAUNCH
     } else {
-        if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
-        else    { if (cgs) LAUNCH(1, 4, false, true); else LAUNCH(1, 4, false, false); }
-    }
+        dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
+        const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
+#define LAUNCH(RPT, CU, HP, CGS)                                                   \
+    do {                                                                           \
+        AQR_TRY(ensure_smem(aqr::trailing_kernel<RPT, CU, HP, CGS>, smem));        \
+        aqr::trailing_kernel<RPT, CU, HP, CGS><<<grid, aqr::kBlock, smem, s>>>(a); \
+    } while (0)
+        if (big) {
+            if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
+            else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
+        } else {
+            if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
+            else    { if (cgs) LAUNCH(1, 4, false, true); else LAUNCH(1, 4, false, false); }
+        }
 #undef LAUNCH
-    if (ev0 && ev1) cudaEventRecord(ev1, s);
-    return launched("trailing_kernel");
+    }
+    timer_end(tix, s);
+    AQR_TRY(launched("trailing_kernel"));
+    if (!tma && a.counters != nullptr)  // generic kernel: totals in a separate launch
+        return launch_rrow_reduce(a.m, ncols, a.partial, a.rout, a.status, s);
+    return AQR_OK;
 }
 
 aqr_status launch_rrow_reduce(int64_t m, int64_t ncols, const double *partial, double *out,
                               const int32_t *status, cudaStream_t s) {
     if (ncols <= 0) return AQR_OK;
     aqr::rrow_reduce_kernel<<<(unsigned)ncols, aqr::kBlock, 0, s>>>(
-        partial, (int32_t)aqr::num_tiles(m), out, status);
+        partial, (int32_t)aqr::num_tiles(m), (int32_t)ncols, out, status);
     return launched("rrow_reduce_kernel");
 }
 
@@ -257,12 +368,14 @@ aqr_status launch_normalize(int64_t m, const double *z, const double *rii, doubl
 inline uint64_t al(uint64_t b) { return (b + 255) & ~uint64_t(255); }
 
 struct Layout {
-    uint64_t status, rt, partial, npart, xvec, pvec, pring, P, X, Z0, total;
+    uint64_t status, counters, rt, partial, npart, xvec, zvec, pvec, pring, P, X, Z0, total;
 };
+
+constexpr uint64_t kNone = ~0ull;
 
 Layout layout(int32_t family, int32_t variant, int32_t orientation, int64_t m, int64_t n) {
     Layout L;
-    const uint64_t ntiles = (uint64_t)aqr::num_tiles(m);
+    const uint64_t ntiles = std::max<uint64_t>((uint64_t)aqr::num_tiles(m), 1);
     const uint64_t mm = (uint64_t)m, nn = (uint64_t)n;
     uint64_t off = 0;
     auto take = [&](uint64_t bytes) {
@@ -271,22 +384,24 @@ Layout layout(int32_t family, int32_t variant, int32_t orientation, int64_t m, i
         return o;
     };
     L.status = take(16 + 4 * nn);
+    L.counters = take(4 * (nn + 8));
     L.rt = take(8 * nn * nn);
-    L.partial = take(8 * nn * std::max<uint64_t>(ntiles, 1));
-    L.npart = take(8 * 3 * std::max<uint64_t>(ntiles, 1));
-    L.xvec = variant != AQR_HP ? take(8 * mm) : ~0ull;
-    L.pvec = (variant == AQR_NAIVE && orientation == AQR_ROW) ? take(8 * mm) : ~0ull;
-    L.pring = (variant == AQR_HP && orientation == AQR_ROW) ? take(8 * 2 * mm) : ~0ull;
-    L.P = orientation == AQR_COL ? take(8 * mm * nn) : ~0ull;
-    L.X = variant == AQR_HP ? take(8 * mm * nn) : ~0ull;
-    L.Z0 = family == AQR_CGS ? take(8 * mm * nn) : ~0ull;
+    L.partial = take(8 * nn * ntiles);
+    L.npart = take(8 * 3 * std::max<uint64_t>((uint64_t)aqr::norm_tiles(m), 1));
+    L.xvec = variant != AQR_HP ? take(8 * mm) : kNone;
+    L.zvec = variant != AQR_HP ? take(8 * mm) : kNone;
+    L.pvec = (variant == AQR_NAIVE && orientation == AQR_ROW) ? take(8 * mm) : kNone;
+    L.pring = (variant == AQR_HP && orientation == AQR_ROW) ? take(8 * 2 * mm) : kNone;
+    L.P = orientation == AQR_COL ? take(8 * mm * nn) : kNone;
+    L.X = variant == AQR_HP ? take(8 * mm * nn) : kNone;
+    L.Z0 = family == AQR_CGS ? take(8 * mm * nn) : kNone;
     L.total = off;
     return L;
 }
 
 template <typename T>
 T *at(void *base, uint64_t off) {
-    return off == ~0ull ? nullptr : reinterpret_cast<T *>(static_cast<char *>(base) + off);
+    return off == kNone ? nullptr : reinterpret_cast<T *>(static_cast<char *>(base) + off);
 }
 
 // ---- the sequencer -------------------------------------------------------------
@@ -294,12 +409,13 @@ T *at(void *base, uint64_t off) {
 struct Run {
     aqr_factor_args *a;
     cudaStream_t s;
-    bool hp, cgs, naive;
+    bool hp, cgs, naive, csr_native;
     int64_t m, n;
     double *W;  // == Q
     int64_t ldw;
     int32_t *status;
-    double *Rt, *partial, *npart, *xvec, *pvec, *pring, *P, *X, *Z0;
+    unsigned *counters;  // [0]: norm, [1 ..]: trailing column groups
+    double *Rt, *partial, *npart, *xvec, *zvec, *pvec, *pring, *P, *X, *Z0;
     int64_t mv = 0;
 
     double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
@@ -311,26 +427,46 @@ struct Run {
         return AQR_OK;
     }
 
-    // z_j (and x_j) receive the deferred update with r_{j-1,j}; then x = A z
-    // (HA/naive) and the norm -> R[j,j], breakdown/flag (normalize(j) lines
-    // 148-160).  Returns the x column used.
-    aqr_status norm_step(int64_t j, const double *pprev_col, const double *&xcol) {
+    aqr::NormOut norm_out(int64_t j) const {
+        aqr::NormOut o;
+        o.npart = npart;
+        o.ntiles = (int32_t)aqr::norm_tiles(m);
+        o.counter = counters;
+        o.tot = nullptr;
+        o.rii = rt(j, j);
+        o.step = j;
+        o.status = status;
+        return o;
+    }
+
+    // Column j receives the deferred projection r_{j-1,j} (z_j and, for HP,
+    // x_j); x = A z (HA/naive); then t = z.x, |z|, |x| -> R[j,j] and the
+    // breakdown / flag record (normalize(j), gram_schmidt.py:148-160).
+    // Returns the columns holding the updated z and x.
+    aqr_status norm_step(int64_t j, const double *pprev_col, const double *&zcol,
+                         const double *&xcol) {
         double *z = col(W, ldw, j);
         const double *qprev = j > 0 ? col(W, ldw, j - 1) : nullptr;
         const double *r = j > 0 ? rt(j - 1, j) : nullptr;
         if (hp) {
             double *x = col(X, m, j);
-            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, x, npart, status, s));
+            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), s));
+            zcol = z;
             xcol = x;
+        } else if (csr_native) {
+            // one fused launch: gather (z - r q), x = A z, z_new, norm, r_jj
+            AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s));
+            ++mv;
+            zcol = zvec;
+            xcol = xvec;
         } else {
-            if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, nullptr, status, s));
+            if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, no_norm(), s));
             AQR_TRY(mv1(z, xvec));  // op.apply(Zw[:, j].copy()), line 151
-            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xvec, npart, status, s));
+            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xvec, norm_out(j), s));
+            zcol = z;
             xcol = xvec;
         }
-        const int32_t nt = (int32_t)aqr::num_tiles(m);
-        aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, s>>>(npart, nt, nullptr, j, rt(j, j), status);
-        return launched("norm_reduce_kernel");
+        return AQR_OK;
     }
 
     aqr::TrailArgs trail(int64_t i, int64_t jbeg, int64_t jend) const {
@@ -348,33 +484,46 @@ struct Run {
         t.ldz0 = m;
         t.rprev = i > 0 ? Rt + (i - 1) * n : nullptr;
         t.partial = partial;
+        t.counters = counters + 1;
+        t.rout = rt(i, jbeg);
         t.status = status;
         return t;
     }
 
     aqr_status row_form() {
         for (int64_t i = 0; i < n; ++i) {
+            const auto hs = std::chrono::steady_clock::now();
             const double *pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
-            const double *xcol = nullptr;
-            AQR_TRY(norm_step(i, pprev, xcol));
+            const double *zcol = nullptr, *xcol = nullptr;
+            AQR_TRY(norm_step(i, pprev, zcol, xcol));
             aqr::TrailArgs t = trail(i, i + 1, n);
             t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
             t.pprev = pprev;
+            t.reverse = (int32_t)(i & 1);
             if (naive) {
                 // q_i first, then p_i = A q_i (lines 161-163)
-                AQR_TRY(launch_normalize(m, col(W, ldw, i), rt(i, i), col(W, ldw, i), nullptr, nullptr, status, s));
+                AQR_TRY(launch_normalize(m, zcol, rt(i, i), col(W, ldw, i), nullptr, nullptr, status, s));
                 AQR_TRY(mv1(col(W, ldw, i), pvec));
                 t.psrc = pvec;
                 t.rii = nullptr;
             } else {
                 t.psrc = xcol;
                 t.rii = rt(i, i);
-                t.zsrc = col(W, ldw, i);
+                t.zsrc = zcol;
                 t.qout = col(W, ldw, i);
                 t.pout = hp ? pring + (i & 1) * m : nullptr;
             }
-            AQR_TRY(launch_trailing(t, hp, cgs, s));
-            AQR_TRY(launch_rrow_reduce(m, n - 1 - i, partial, rt(i, i + 1), status, s));
+            {
+                static const bool dbg = std::getenv("AQR_DEBUG_TIMING") != nullptr;
+                const auto h0 = std::chrono::steady_clock::now();
+                AQR_TRY(launch_trailing(t, hp, cgs, s));
+                if (dbg) {
+                    const auto h1 = std::chrono::steady_clock::now();
+                    std::fprintf(stderr, "  step %ld trailing launch host %.1f us, norm-step host %.1f us\n", (long)i,
+                                 std::chrono::duration<double, std::micro>(h1 - h0).count(),
+                                 std::chrono::duration<double, std::micro>(h0 - hs).count());
+                }
+            }
         }
         return AQR_OK;
     }
@@ -388,16 +537,15 @@ struct Run {
                 t.psrc = col(P, m, i);
                 t.rii = nullptr;
                 AQR_TRY(launch_trailing(t, hp, cgs, s));
-                AQR_TRY(launch_rrow_reduce(m, 1, partial, rt(i, j), status, s));
             }
             const double *pprev = (hp && j > 0) ? col(P, m, j - 1) : nullptr;
-            const double *xcol = nullptr;
-            AQR_TRY(norm_step(j, pprev, xcol));  // normalize(j), line 171
+            const double *zcol = nullptr, *xcol = nullptr;
+            AQR_TRY(norm_step(j, pprev, zcol, xcol));  // normalize(j), line 171
             if (naive) {
-                AQR_TRY(launch_normalize(m, col(W, ldw, j), rt(j, j), col(W, ldw, j), nullptr, nullptr, status, s));
+                AQR_TRY(launch_normalize(m, zcol, rt(j, j), col(W, ldw, j), nullptr, nullptr, status, s));
                 AQR_TRY(mv1(col(W, ldw, j), col(P, m, j)));
             } else {
-                AQR_TRY(launch_normalize(m, col(W, ldw, j), rt(j, j), col(W, ldw, j), xcol, col(P, m, j), status, s));
+                AQR_TRY(launch_normalize(m, zcol, rt(j, j), col(W, ldw, j), xcol, col(P, m, j), status, s));
             }
         }
         return AQR_OK;
@@ -414,26 +562,40 @@ uint64_t aqr_launch_count(void) { return g_launches.load(std::memory_order_relax
 aqr_status aqr_trailing_timer_enable(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_timer.mu);
     g_timer.enabled = enable != 0;
+    if (g_timer.enabled) {
+        g_timer.recs.clear();
+        g_timer.used = 0;
+    }
+    return AQR_OK;
+}
+
+aqr_status aqr_kernel_timer_read(int32_t slot, int64_t *launches, double *ms, double *bytes) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    double total = 0.0, b = 0.0;
+    int64_t n = 0;
+    for (const auto &r : g_timer.recs) {
+        if (r.slot != slot) continue;
+        AQR_CUDA(cudaEventSynchronize(r.e1));
+        float dt = 0.f;
+        AQR_CUDA(cudaEventElapsedTime(&dt, r.e0, r.e1));
+        total += dt;
+        b += r.bytes;
+        ++n;
+    }
+    if (launches) *launches = n;
+    if (ms) *ms = total;
+    if (bytes) *bytes = b;
     return AQR_OK;
 }
 
 aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double *bytes) {
+    AQR_TRY(aqr_kernel_timer_read(0, launches, ms, bytes));
     std::lock_guard<std::mutex> lk(g_timer.mu);
-    double total = 0.0;
-    for (size_t k = 0; k + 1 < g_timer.used; k += 2) {
-        AQR_CUDA(cudaEventSynchronize(g_timer.pool[k + 1]));
-        float dt = 0.f;
-        AQR_CUDA(cudaEventElapsedTime(&dt, g_timer.pool[k], g_timer.pool[k + 1]));
-        total += dt;
-    }
-    if (launches) *launches = g_timer.launches;
-    if (ms) *ms = total;
-    if (bytes) *bytes = g_timer.bytes;
+    g_timer.recs.clear();
     g_timer.used = 0;
-    g_timer.bytes = 0.0;
-    g_timer.launches = 0;
     return AQR_OK;
 }
+
 int32_t aqr_abi_version(void) { return AQR_ABI_VERSION; }
 int64_t aqr_tile_rows(int64_t m) { return aqr::tile_rows(m); }
 int64_t aqr_num_tiles(int64_t m) { return aqr::num_tiles(m); }
@@ -461,7 +623,7 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
     const int64_t m = a->m, n = a->n;
     if (n < 1 || m < n) return set_err(AQR_EDIM, "need m >= n >= 1");
     if (!a->op || a->op->m != m) return set_err(AQR_EDIM, "operator dimension does not match Z");
-    if (n > (int64_t)INT32_MAX || m > ((int64_t)1 << 40)) return set_err(AQR_EARG, "size out of range");
+    if (n > (int64_t)INT32_MAX / 2 || m > ((int64_t)1 << 40)) return set_err(AQR_EARG, "size out of range");
     if (!a->Z || !a->Q || !a->R || a->ldz < m || a->ldq < m || a->ldr < n)
         return set_err(AQR_EARG, "bad Z/Q/R pointer or leading dimension");
     const Layout L = layout(a->family, a->variant, a->orientation, m, n);
@@ -474,16 +636,19 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
     r.hp = a->variant == AQR_HP;
     r.naive = a->variant == AQR_NAIVE;
     r.cgs = a->family == AQR_CGS;
+    r.csr_native = a->op->kind == AQR_OP_CSR;
     r.m = m;
     r.n = n;
     r.W = a->Q;
     r.ldw = a->ldq;
     void *ws = a->workspace;
     r.status = at<int32_t>(ws, L.status);
+    r.counters = at<unsigned>(ws, L.counters);
     r.Rt = at<double>(ws, L.rt);
     r.partial = at<double>(ws, L.partial);
     r.npart = at<double>(ws, L.npart);
     r.xvec = at<double>(ws, L.xvec);
+    r.zvec = at<double>(ws, L.zvec);
     r.pvec = at<double>(ws, L.pvec);
     r.pring = at<double>(ws, L.pring);
     r.P = at<double>(ws, L.P);
@@ -494,6 +659,7 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
     if (a->Z != a->Q)  // Zw = Z.copy(order="F"), line 131
         AQR_CUDA(cudaMemcpy2DAsync(a->Q, a->ldq * 8, a->Z, a->ldz * 8, m * 8, n, cudaMemcpyDeviceToDevice, s));
     AQR_TRY(aqr_status_init(r.status, n, stream));
+    AQR_CUDA(cudaMemsetAsync(r.counters, 0, 4 * (size_t)(n + 8), s));
     AQR_CUDA(cudaMemsetAsync(r.Rt, 0, 8 * (size_t)n * n, s));
     if (r.cgs)  // Z0, line 132
         AQR_CUDA(cudaMemcpy2DAsync(r.Z0, m * 8, a->Q, a->ldq * 8, m * 8, n, cudaMemcpyDeviceToDevice, s));
@@ -501,12 +667,21 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
         AQR_TRY(op_apply(a->op, n, a->Q, a->ldq, r.X, m, s));
         r.mv += n;
     }
+    static const bool debug_timing = std::getenv("AQR_DEBUG_TIMING") != nullptr;
+    const auto t_loop = std::chrono::steady_clock::now();
     AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
     aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, r.Rt, a->R, a->ldr);
     AQR_TRY(launched("finalize_r_kernel"));
     std::vector<int32_t> st((16 + 4 * n) / 4);
     AQR_CUDA(cudaMemcpyAsync(st.data(), r.status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
+    const auto t_enq = std::chrono::steady_clock::now();
     AQR_CUDA(cudaStreamSynchronize(s));
+    if (debug_timing) {
+        const auto t_end = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "aqr_gs_factor: enqueue loop %.1f us, wait %.1f us\n",
+                     std::chrono::duration<double, std::micro>(t_enq - t_loop).count(),
+                     std::chrono::duration<double, std::micro>(t_end - t_enq).count());
+    }
     a->mv_count = r.mv;
     if (a->flagged_host) std::memcpy(a->flagged_host, st.data() + 4, 4 * n);
     if (st[0] >= 0) {
@@ -524,8 +699,8 @@ aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientati
                               int64_t *fail_col, double *fail_val, int32_t *flagged_host,
                               int64_t *mv_count) {
     if (n < 1 || m < n) return set_err(AQR_EDIM, "need m >= n >= 1");
-    if (op_kind == AQR_OP_CSR && nnz >= ((int64_t)1 << 31))
-        return set_err(AQR_EARG, "nnz >= 2^31 does not fit the int32 CSR layout");
+    if (op_kind == AQR_OP_CSR && (nnz >= ((int64_t)1 << 31) || m >= ((int64_t)1 << 31)))
+        return set_err(AQR_EARG, "nnz/m >= 2^31 does not fit the int32 CSR layout");
     cudaStream_t s;
     AQR_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     std::vector<void *> bufs;
@@ -672,19 +847,21 @@ aqr_status aqr_csr_matvec(int64_t m, const int32_t *indptr, const int32_t *indic
     op.indptr = indptr;
     op.indices = indices;
     op.data = data;
-    op.spmv_lanes = 8;  // explicit: no nnz needed to pick the lane count
     return aqr_op_apply(&op, 1, x, m, y, m, stream);
 }
 
 aqr_status aqr_step_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
                                     const double *pprev, const double *r_dev, const double *xnorm,
                                     double *npart, const int32_t *status, void *stream) {
-    return launch_col_update_norm(m, z, qprev, x, pprev, r_dev, xnorm, npart, status, S(stream));
+    aqr::NormOut o = no_norm();
+    o.npart = npart;
+    o.status = const_cast<int32_t *>(status);
+    return launch_col_update_norm(m, z, qprev, x, pprev, r_dev, xnorm, o, S(stream));
 }
 
 aqr_status aqr_step_norm_reduce(int64_t m, const double *npart, double *tot, const int32_t *status,
                                 void *stream) {
-    aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, S(stream)>>>(npart, (int32_t)aqr::num_tiles(m), tot, 0,
+    aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, S(stream)>>>(npart, (int32_t)aqr::norm_tiles(m), tot, 0,
                                                             nullptr, const_cast<int32_t *>(status));
     return launched("norm_reduce_kernel");
 }
@@ -704,13 +881,13 @@ aqr_status aqr_step_trailing(int64_t m, int64_t i, int64_t jbeg, int64_t jend, d
                              const double *pprev, const double *rprev, const double *psrc,
                              const double *rii, double *pout, const double *zsrc, double *qout,
                              double *partial, const int32_t *status, void *stream) {
-    (void)i;
     aqr::TrailArgs t;
     std::memset(&t, 0, sizeof t);
     t.m = m;
     t.ntiles = (int32_t)aqr::num_tiles(m);
     t.jbeg = (int32_t)jbeg;
     t.jend = (int32_t)jend;
+    t.reverse = (int32_t)(i & 1);
     t.W = W;
     t.ldw = ldw;
     t.X = X;

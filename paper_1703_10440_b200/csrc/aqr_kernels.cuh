@@ -1,16 +1,25 @@
 // aqr_kernels.cuh -- sm_100a device kernels of the A-orthogonal MGS hot path.
 //
 // Layout: column-major fp64 matrices with explicit leading dimension; CSR
-// with int32 indptr/indices and fp64 values.  Reductions are atomic-free
-// and depend only on (m, launch geometry fixed by m): rows are cut into
-// tiles of tile_rows(m) rows, each tile partial is a fixed function of the
-// tile's rows (per-thread ascending order, warp xor-butterfly 16..1, warps
-// summed in ascending order) and tile partials are summed in a fixed order
-// by *_reduce kernels.  Column grouping (blockIdx.y) never changes a tile
-// partial, so the column-oriented schedule (one trailing column per launch)
-// and the row-oriented schedule (all trailing columns per launch) produce
-// bitwise-identical R and Q, the property the reference guarantees for its
-// sequential loops (gram_schmidt.py:19-21).
+// with int32 indptr/indices and fp64 values.
+//
+// Determinism.  Every reduction is atomic-free in its arithmetic and depends
+// only on m (never on the step, variant, orientation, grid size or column
+// grouping):
+//   * rows are cut into tiles of tile_rows(m) = 256 * RPT rows; thread k of a
+//     tile owns rows k + 256 u (u = 0..RPT-1), accumulates them in ascending u
+//     with fma, the warp reduces with an xor butterfly (16, 8, 4, 2, 1) and the
+//     8 warps are added in ascending order -> one partial per (tile, column);
+//   * the norm partials (z.x, z.z, x.x) use 256-row tiles (block tree);
+//   * a column total over tiles is block_totals(): thread k adds the tiles
+//     k, k+256, k+512, ... in ascending order, then the warp xor butterfly
+//     and the 8 warps in ascending order.
+// Every kernel that produces or consumes these partials uses exactly these
+// functions, so the row- and column-oriented schedules, the native and the
+// callback operator routes and the step API all return bitwise-identical
+// factors, the property the reference guarantees for its sequential loops
+// (gram_schmidt.py:19-21).  Atomics are used only as completion tickets
+// ("last CTA finishes"), never to accumulate values.
 //
 // Elementwise updates follow the reference exactly: z -= a*q is a rounded
 // multiply then a rounded subtract (__dmul_rn/__dsub_rn, no FMA contraction;
@@ -27,8 +36,7 @@ namespace aqr {
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 
-// Rows per thread of the reduction tile.  Depends on m only (never on the
-// step, the variant or the orientation).
+// Rows per thread of the reduction tile: depends on m only.
 __host__ __device__ inline int rows_per_thread(int64_t m) {
     return m >= (int64_t)2048 * 148 ? 8 : 1;
 }
@@ -37,6 +45,10 @@ __host__ __device__ inline int64_t num_tiles(int64_t m) {
     const int64_t t = tile_rows(m);
     return (m + t - 1) / t;
 }
+// The norm partials (z.x, z.z, x.x) use 256-row tiles (thread k owns row k,
+// block tree), so the fine-grained SpMV can emit them; their totals are
+// block_totals over ceil(m / 256) partials.
+__host__ __device__ inline int64_t norm_tiles(int64_t m) { return (m + kBlock - 1) / kBlock; }
 
 __device__ __forceinline__ bool failed(const int32_t *status) {
     return status != nullptr && *(volatile const int32_t *)status >= 0;
@@ -48,7 +60,7 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Fixed-order block sum; every thread returns the same value.
+// Fixed-order block sum over kBlock threads; every thread returns the value.
 __device__ __forceinline__ double block_sum(double v, double *smem /* kWarps */) {
     v = warp_sum(v);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -61,14 +73,284 @@ __device__ __forceinline__ double block_sum(double v, double *smem /* kWarps */)
     return s;
 }
 
+// Canonical total of NC partial arrays p + c * stride (c < NC), each of n
+// tile partials: thread k (k < 256) adds the tiles k, k+256, k+512, ... in
+// ascending order, the warp reduces with the xor butterfly and the 8 warps
+// are added in ascending order.  Called by threads 0..255 of the CTA (the
+// other threads must not call it); `bar` is the barrier those 256 threads
+// share (__syncthreads, or a named barrier in warp-specialized kernels).
+// Loads are issued 4 per chain ahead of the adds, so even 8192 tiles cost
+// only a few dependent L2 round trips.
+template <int NC, typename Bar>
+__device__ __forceinline__ void block_totals(const double *p, int64_t stride, int32_t n,
+                                             double *out /* smem or global, NC */,
+                                             double *sm /* NC * kWarps */, Bar bar) {
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    for (int t0 = threadIdx.x; t0 < n; t0 += 4 * kBlock) {
+        double v[NC][4];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const int t = t0 + h * kBlock;
+                v[c][h] = t < n ? __ldcg(p + c * stride + t) : 0.0;
+            }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                if (t0 + h * kBlock < n) acc[c] = __dadd_rn(acc[c], v[c][h]);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double w = warp_sum(acc[c]);
+        if (lane == 0) sm[c * kWarps + warp] = w;
+    }
+    bar();
+    if (threadIdx.x < NC) {
+        double s = sm[threadIdx.x * kWarps];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, sm[threadIdx.x * kWarps + w]);
+        out[threadIdx.x] = s;
+    }
+    bar();
+}
+
+struct SyncAll {
+    __device__ void operator()() const { __syncthreads(); }
+};
+
+// Status block: int32 fail column at [0], double fail value at byte 8,
+// int32 flags[n] at byte 16.
+__device__ __forceinline__ void norm_finish_dev(int64_t i, double t, double zz, double xx,
+                                                double *rii, int32_t *status) {
+    if (!(t > 0.0) || !isfinite(t)) {  // gram_schmidt.py:153-154
+        if (status[0] < 0) {
+            status[0] = (int32_t)i;
+            *reinterpret_cast<double *>(status + 2) = t;
+        }
+        return;
+    }
+    const double unit_roundoff = 1.1102230246251565e-16;  // 2**-53, gram_schmidt.py:33
+    const double nz = sqrt(zz), nx = sqrt(xx);
+    if (t < 100.0 * unit_roundoff * nz * nx) status[4 + i] = 1;  // gram_schmidt.py:155-158
+    *rii = sqrt(t);                                               // gram_schmidt.py:159
+}
+
+// Block-wide "am I the last CTA" ticket (all kBlock threads call it after
+// writing their partials).  Resets the counter when it fires.
+__device__ __forceinline__ bool last_block(unsigned *counter, unsigned expected) {
+    __shared__ unsigned ticket;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+    __syncthreads();
+    const bool last = ticket == expected - 1;
+    if (last) {
+        __threadfence();
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+    return last;
+}
+
+// The three norm partials of a tile -> npart, and the last CTA finishes:
+// totals (tot, optional) and the breakdown / flag / r_ii record.
+struct NormOut {
+    double *npart;  // [3 * ntiles] or nullptr
+    int32_t ntiles;
+    unsigned *counter;  // nullptr: no finish in-kernel
+    double *tot;        // optional totals
+    double *rii;        // optional: finish (breakdown check, flag, sqrt)
+    int64_t step;
+    int32_t *status;
+};
+
+// Norm partials of 256-row tiles.  norm_sub_partial(g, ...) is called by
+// every thread for each of NT consecutive tiles tile0 + g (this thread's
+// (z.x, z.z, x.x) terms of row (tile0+g)*256 + k, zero past m);
+// norm_tiles_finish<NT>() then forms the NT partials with the block_sum tree
+// (warp xor butterfly, warps in ascending order), one barrier pair.
+__device__ __forceinline__ void norm_sub_partial(int g, double t, double zz, double xx,
+                                                 double *sm /* [NT*3*kWarps] */) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    t = warp_sum(t);
+    zz = warp_sum(zz);
+    xx = warp_sum(xx);
+    if (lane == 0) {
+        sm[(g * 3 + 0) * kWarps + warp] = t;
+        sm[(g * 3 + 1) * kWarps + warp] = zz;
+        sm[(g * 3 + 2) * kWarps + warp] = xx;
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void norm_tiles_finish(const NormOut &o, int64_t tile0, double *sm) {
+    __syncthreads();
+    if (threadIdx.x < 3 * NT) {
+        const int g = threadIdx.x / 3, k = threadIdx.x % 3;
+        if (tile0 + g < o.ntiles) {
+            double s = sm[(g * 3 + k) * kWarps];
+#pragma unroll
+            for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, sm[(g * 3 + k) * kWarps + w]);
+            o.npart[(int64_t)k * o.ntiles + tile0 + g] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// After a CTA wrote all its tiles' partials: the last CTA of the grid forms
+// the totals (block_totals) and finishes the column (one ticket per CTA).
+// Called by all kBlock threads.
+__device__ __forceinline__ void norm_last_cta(const NormOut &o) {
+    if (o.counter == nullptr) return;
+    if (!last_block(o.counter, gridDim.x)) return;
+    __shared__ double tot[3];
+    __shared__ double sm3[3 * kWarps];
+    block_totals<3>(o.npart, o.ntiles, o.ntiles, tot, sm3, SyncAll());
+    if (threadIdx.x == 0) {
+        if (o.tot) {
+            o.tot[0] = tot[0];
+            o.tot[1] = tot[1];
+            o.tot[2] = tot[2];
+        }
+        if (o.rii) norm_finish_dev(o.step, tot[0], tot[1], tot[2], o.rii, o.status);
+    }
+}
+
 // ---------------------------------------------------------------------------
-// Fused trailing pass (one MGS step, row-oriented look-ahead schedule)
+// Column update (deferred step i-1 projection of column i) + norm partials
+// ---------------------------------------------------------------------------
+struct ColArgs {
+    int64_t m;
+    double *z;
+    const double *qprev;
+    double *x;  // HP: carried column, updated in place (nullptr otherwise)
+    const double *pprev;
+    const double *r;      // r_{i-1,i} (nullptr: no update)
+    const double *xnorm;  // x used for the norm partials when x == nullptr
+    NormOut out;          // out.npart == nullptr: update only
+};
+
+// Grid-stride over groups of kColTiles consecutive 256-row norm tiles
+// (thread k owns row k of each; all loads of a group in flight together),
+// one barrier pair per group, one completion ticket per CTA.
+constexpr int kColTiles = 4;
+__global__ void __launch_bounds__(kBlock) col_update_norm_kernel(ColArgs a) {
+    if (failed(a.out.status)) return;
+    __shared__ double sm[kColTiles * 3 * kWarps];
+    const bool upd = a.r != nullptr;
+    const double rj = upd ? *a.r : 0.0;
+    const int64_t ntiles = (a.m + kBlock - 1) / kBlock;
+    for (int64_t tile0 = (int64_t)blockIdx.x * kColTiles; tile0 < ntiles;
+         tile0 += (int64_t)gridDim.x * kColTiles) {
+        double z[kColTiles], xv[kColTiles], q[kColTiles], pp[kColTiles];
+#pragma unroll
+        for (int g = 0; g < kColTiles; ++g) {  // loads first
+            const int64_t r = (tile0 + g) * kBlock + threadIdx.x;
+            const bool ok = r < a.m;
+            z[g] = ok ? a.z[r] : 0.0;
+            q[g] = (ok && upd) ? a.qprev[r] : 0.0;
+            xv[g] = ok ? (a.x ? a.x[r] : (a.xnorm ? a.xnorm[r] : 0.0)) : 0.0;
+            pp[g] = (ok && upd && a.x) ? a.pprev[r] : 0.0;
+        }
+#pragma unroll
+        for (int g = 0; g < kColTiles; ++g) {
+            const int64_t r = (tile0 + g) * kBlock + threadIdx.x;
+            const bool ok = r < a.m;
+            if (upd) {
+                z[g] = __dsub_rn(z[g], __dmul_rn(rj, q[g]));
+                if (ok) a.z[r] = z[g];
+                if (a.x) {
+                    xv[g] = __dsub_rn(xv[g], __dmul_rn(rj, pp[g]));
+                    if (ok) a.x[r] = xv[g];
+                }
+            }
+            if (a.out.npart != nullptr)
+                norm_sub_partial(g, ok ? fma(z[g], xv[g], 0.0) : 0.0, ok ? fma(z[g], z[g], 0.0) : 0.0,
+                                 ok ? fma(xv[g], xv[g], 0.0) : 0.0, sm);
+        }
+        if (a.out.npart != nullptr) norm_tiles_finish<kColTiles>(a.out, tile0, sm);
+    }
+    if (a.out.npart != nullptr) norm_last_cta(a.out);
+}
+
+// Standalone totals of the norm partials (step API / multi-GPU driver).
+__global__ void __launch_bounds__(kBlock)
+    norm_reduce_kernel(const double *npart, int32_t ntiles, double *tot, int64_t i, double *rii,
+                       int32_t *status) {
+    if (failed(status)) return;
+    __shared__ double t3[3];
+    __shared__ double sm3[3 * kWarps];
+    block_totals<3>(npart, ntiles, ntiles, t3, sm3, SyncAll());
+    if (threadIdx.x == 0) {
+        if (tot) {
+            tot[0] = t3[0];
+            tot[1] = t3[1];
+            tot[2] = t3[2];
+        }
+        if (rii) norm_finish_dev(i, t3[0], t3[1], t3[2], rii, status);
+    }
+}
+
+__global__ void norm_finish_kernel(int64_t i, const double *tot, double *rii, int32_t *status) {
+    if (failed(status)) return;
+    norm_finish_dev(i, tot[0], tot[1], tot[2], rii, status);
+}
+
+// Standalone column totals: block c reduces column c (block_totals).
+__global__ void __launch_bounds__(kBlock)
+    rrow_reduce_kernel(const double *partial, int32_t ntiles, int32_t ncols, double *out,
+                       const int32_t *status) {
+    if (failed(status)) return;
+    __shared__ double sm[kWarps];
+    (void)ncols;
+    block_totals<1>(partial + (int64_t)blockIdx.x * ntiles, ntiles, ntiles, out + blockIdx.x, sm,
+                    SyncAll());
+}
+
+// q = z / rii ; p = x / rii  (normalize(j), gram_schmidt.py:159-165)
+__global__ void __launch_bounds__(kBlock)
+    normalize_kernel(int64_t m, const double *z, const double *rii, double *q, const double *x,
+                     double *p, const int32_t *status) {
+    if (failed(status)) return;
+    const double r = *rii;
+    for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * kBlock) {
+        q[i] = z[i] / r;
+        if (p) p[i] = x[i] / r;
+    }
+}
+
+__global__ void finalize_r_kernel(int64_t n, const double *Rt, double *R, int64_t ldr) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * n) return;
+    const int64_t i = idx % n, j = idx / n;  // R column-major: (i, j)
+    R[i + j * ldr] = i <= j ? Rt[i * n + j] : 0.0;
+}
+
+__global__ void status_init_kernel(int32_t *status, int64_t n) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx == 0) {
+        status[0] = -1;
+        status[1] = 0;
+        *reinterpret_cast<double *>(status + 2) = 0.0;
+    }
+    if (idx < n) status[4 + idx] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Fused trailing pass, generic (direct loads; any m)
 // ---------------------------------------------------------------------------
 struct TrailArgs {
     int64_t m;
     int32_t ntiles;
-    int32_t cpg;  // columns per blockIdx.y group
+    int32_t cpg;     // columns per group
+    int32_t ngroups;
     int32_t jbeg, jend;
+    int32_t reverse;  // walk the work items backwards (L2 reuse across steps)
     double *W;
     int64_t ldw;
     double *X;  // HP carried A z (nullptr otherwise)
@@ -80,12 +362,35 @@ struct TrailArgs {
     const double *rprev;  // r_{i-1, j} = rprev[j] (row i-1 of row-major Rt)
     const double *psrc;   // p_i = psrc / *rii  (or psrc itself when rii == nullptr)
     const double *rii;
-    double *pout;         // store p_i (blockIdx.y == 0)
+    double *pout;         // store p_i (group 0)
     const double *zsrc;   // z_i
-    double *qout;         // store q_i = z_i / *rii (blockIdx.y == 0)
+    double *qout;         // store q_i = z_i / *rii (group 0)
     double *partial;      // [(j - jbeg) * ntiles + tile]
+    unsigned *counters;   // per group; nullptr: no in-kernel totals
+    double *rout;         // totals: rout[j - jbeg] (row i of Rt from column jbeg)
     const int32_t *status;
 };
+
+// Load the step vectors of one tile into registers; group 0 stores q_i/p_i.
+template <int RPT, bool HP>
+__device__ __forceinline__ void trail_vectors(const TrailArgs &a, int64_t row0, bool store,
+                                              double *q, double *p, double *pp) {
+    const bool upd = a.qprev != nullptr;
+    const double rii = a.rii ? *a.rii : 1.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t r = row0 + (int64_t)u * kBlock;
+        const bool ok = r < a.m;
+        const double ps = ok ? a.psrc[r] : 0.0;
+        p[u] = a.rii ? ps / rii : ps;
+        q[u] = (ok && upd) ? a.qprev[r] : 0.0;
+        pp[u] = (HP && ok && upd) ? a.pprev[r] : 0.0;
+        if (store && ok) {
+            if (a.qout) a.qout[r] = a.zsrc[r] / rii;
+            if (a.pout) a.pout[r] = p[u];
+        }
+    }
+}
 
 template <int RPT, int CU, bool HP, bool CGS>
 __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
@@ -96,24 +401,13 @@ __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
     const int cbeg = a.jbeg + blockIdx.y * a.cpg;
     const int cend = min(a.jend, cbeg + a.cpg);
     const bool upd = a.qprev != nullptr;
-    const double rii = a.rii ? *a.rii : 1.0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     double q[RPT], p[RPT], pp[RPT];
+    trail_vectors<RPT, HP>(a, row0, blockIdx.y == 0, q, p, pp);
     bool ok[RPT];
 #pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-        const int64_t r = row0 + (int64_t)u * kBlock;
-        ok[u] = r < a.m;
-        const double ps = ok[u] ? a.psrc[r] : 0.0;
-        p[u] = a.rii ? ps / rii : ps;
-        q[u] = (ok[u] && upd) ? a.qprev[r] : 0.0;
-        pp[u] = (HP && ok[u] && upd) ? a.pprev[r] : 0.0;
-        if (blockIdx.y == 0 && ok[u]) {
-            if (a.qout) a.qout[r] = a.zsrc[r] / rii;
-            if (a.pout) a.pout[r] = p[u];
-        }
-    }
+    for (int u = 0; u < RPT; ++u) ok[u] = row0 + (int64_t)u * kBlock < a.m;
 
     for (int j0 = cbeg; j0 < cend; j0 += CU) {
         double z[CU][RPT], x[CU][RPT], rj[CU];
@@ -165,153 +459,281 @@ __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
         for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsum[w * a.cpg + c]);
         a.partial[(int64_t)(cbeg - a.jbeg + c) * a.ntiles + tile] = s;
     }
-}
-
-// out[c] = sum over tiles of partial[c * ntiles + tile], fixed order.
-__global__ void __launch_bounds__(kBlock)
-    rrow_reduce_kernel(const double *partial, int32_t ntiles, double *out, const int32_t *status) {
-    if (failed(status)) return;
-    __shared__ double sm[kWarps];
-    const double *p = partial + (int64_t)blockIdx.x * ntiles;
-    double s = 0.0;
-    for (int t = threadIdx.x; t < ntiles; t += kBlock) s = __dadd_rn(s, p[t]);
-    s = block_sum(s, sm);
-    if (threadIdx.x == 0) out[blockIdx.x] = s;
+    // totals: rrow_reduce_kernel (one CTA per column) follows this launch
 }
 
 // ---------------------------------------------------------------------------
-// Column update (deferred step i-1 projection of column i) + norm partials
+// Fused trailing pass, TMA-bulk pipelined (m >= 2048*148: RPT = 8, tiles of
+// 2048 rows = 16 KB per column).  Persistent: 2 CTAs per SM.  The step's
+// U = ntiles * t (tile, column) units are split into equal contiguous ranges,
+// one per CTA (unit u -> tile u / t, column jbeg + u % t), so every CTA moves
+// the same number of bytes and re-loads the step vectors only when its range
+// enters a new tile.  One producer warp streams the CTA's (tile, column)
+// blocks into a ring of shared-memory stages with cp.async.bulk + mbarrier
+// transaction counts (L2 evict-first: the stream must not evict the operator
+// and the step vectors); 8 consumer warps apply the deferred update, write
+// the column back (streaming stores) and accumulate p_i . z_j with the
+// canonical tile-partial structure (thread k owns rows k + 256 u).  The r row
+// totals are formed at the end by the last ceil(t / 32) CTAs to finish, which
+// wait for the whole grid (all CTAs are co-resident) -- one fence per CTA.
 // ---------------------------------------------------------------------------
-struct ColArgs {
-    int64_t m;
-    int32_t ntiles;
-    double *z;
-    const double *qprev;
-    double *x;  // HP: carried column, updated in place (nullptr otherwise)
-    const double *pprev;
-    const double *r;      // r_{i-1,i} (nullptr: no update)
-    const double *xnorm;  // x used for the norm partials (== x for HP)
-    double *npart;        // [3 * ntiles] or nullptr
-    const int32_t *status;
+constexpr int kTmaRpt = 8;
+constexpr int kTmaTileRows = kBlock * kTmaRpt;  // 2048
+constexpr int kTmaTileBytes = kTmaTileRows * 8;  // 16 KB
+constexpr int kTmaThreads = kBlock + 32;         // + producer warp
+constexpr int kTmaMaxCols = 256;                 // rprev / run partials staged in smem
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+template <bool HINT>
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t pol) {
+    if (HINT)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar))
+            : "memory");
+}
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+struct ConsumerBar {
+    __device__ void operator()() const { consumer_bar(); }
 };
 
-template <int RPT>
-__global__ void __launch_bounds__(kBlock) col_update_norm_kernel(ColArgs a) {
+template <bool HP, bool CGS>
+struct TmaCfg {
+    static constexpr int kArrays = 1 + (HP ? 1 : 0) + (CGS ? 1 : 0);
+    static constexpr int kStageBytes = kArrays * kTmaTileBytes;
+    static constexpr int kStages = kArrays == 1 ? 5 : (kArrays == 2 ? 3 : 2);
+    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 2 * kStages * 8 +
+                                    (size_t)kTmaMaxCols * 8 /* rprev */ +
+                                    (size_t)kWarps * kTmaMaxCols * 8 /* run partials */ + 64;
+};
+
+// The CTA's unit range walked as runs of columns inside one tile, forwards
+// or backwards; the producer and the consumers walk the same sequence.
+struct RunWalker {
+    int64_t u0, u1, u;
+    int tcols;
+    bool rev;
+    __device__ RunWalker(int64_t units, int tcols_, bool rev_) : tcols(tcols_), rev(rev_) {
+        u0 = units * blockIdx.x / gridDim.x;
+        u1 = units * (blockIdx.x + 1) / gridDim.x;
+        u = rev ? u1 : u0;
+    }
+    // next run: tile, columns [c0, c1) (relative to jbeg); false when done
+    __device__ bool next(int64_t &tile, int &c0, int &c1) {
+        if (!rev) {
+            if (u >= u1) return false;
+            tile = u / tcols;
+            c0 = (int)(u % tcols);
+            { const int64_t e = c0 + (u1 - u); c1 = e < tcols ? (int)e : tcols; }
+            u += c1 - c0;
+        } else {
+            if (u <= u0) return false;
+            tile = (u - 1) / tcols;
+            c1 = (int)((u - 1) % tcols) + 1;
+            { const int64_t b = c1 - (u - u0); c0 = b > 0 ? (int)b : 0; }
+            u -= c1 - c0;
+        }
+        return true;
+    }
+};
+
+template <bool HP, bool CGS, bool HINT>
+__global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs a) {
+    using C = TmaCfg<HP, CGS>;
     if (failed(a.status)) return;
-    __shared__ double sm[kWarps];
-    const int64_t row0 = (int64_t)blockIdx.x * (kBlock * RPT) + threadIdx.x;
-    const bool upd = a.r != nullptr;
-    const double rj = upd ? *a.r : 0.0;
-    double t = 0.0, zz = 0.0, xx = 0.0;
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-        const int64_t r = row0 + (int64_t)u * kBlock;
-        if (r >= a.m) continue;
-        double z = a.z[r];
-        if (upd) {
-            z = __dsub_rn(z, __dmul_rn(rj, a.qprev[r]));
-            a.z[r] = z;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double *stage_buf = reinterpret_cast<double *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)C::kStages * C::kStageBytes);
+    uint64_t *empty = full + C::kStages;
+    double *rsm = reinterpret_cast<double *>(empty + C::kStages);  // [kTmaMaxCols]
+    double *wsum = rsm + kTmaMaxCols;                               // [kWarps][kTmaMaxCols]
+    __shared__ unsigned s_ticket;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = a.jend - a.jbeg;
+    const int tcols = t > 0 ? t : 1;  // t == 0: one vector-only unit per tile (q_i, p_i)
+    const int64_t units = (int64_t)a.ntiles * tcols;
+    const bool upd = a.qprev != nullptr;
+    const int64_t full_tiles = a.m / kTmaTileRows;  // tiles streamed by TMA
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kWarps);
         }
-        double xv = 0.0;
-        if (a.x) {
-            xv = a.x[r];
-            if (upd) {
-                xv = __dsub_rn(xv, __dmul_rn(rj, a.pprev[r]));
-                a.x[r] = xv;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int c = threadIdx.x; c < t; c += kTmaThreads) rsm[c] = upd ? a.rprev[a.jbeg + c] : 0.0;
+    __syncthreads();
+
+    if (warp == kWarps) {  // ---------------- producer warp ----------------
+        if (lane == 0 && t > 0) {
+            const uint64_t pol = policy_evict_first();
+            uint32_t it = 0;
+            RunWalker wk(units, tcols, a.reverse != 0);
+            int64_t tile;
+            int c0, c1;
+            while (wk.next(tile, c0, c1)) {
+                if (tile >= full_tiles) continue;
+                const int64_t rbase = tile * kTmaTileRows;
+                for (int cc = 0; cc < c1 - c0; ++cc, ++it) {
+                    const int j = a.jbeg + (a.reverse ? c1 - 1 - cc : c0 + cc);
+                    const int s = it % C::kStages;
+                    const uint32_t ph = (it / C::kStages) & 1;
+                    mbar_wait(empty + s, ph ^ 1);
+                    mbar_expect_tx(full + s, C::kStageBytes);
+                    double *dst = stage_buf + (size_t)s * (C::kStageBytes / 8);
+                    bulk_g2s<HINT>(dst, a.W + (int64_t)j * a.ldw + rbase, kTmaTileBytes, full + s, pol);
+                    if (HP)
+                        bulk_g2s<HINT>(dst + kTmaTileRows, a.X + (int64_t)j * a.ldx + rbase,
+                                       kTmaTileBytes, full + s, pol);
+                    if (CGS)
+                        bulk_g2s<HINT>(dst + (C::kArrays - 1) * kTmaTileRows,
+                                       a.Z0 + (int64_t)j * a.ldz0 + rbase, kTmaTileBytes, full + s, pol);
+                }
             }
-        } else if (a.xnorm) {
-            xv = a.xnorm[r];
         }
-        t = fma(z, xv, t);
-        zz = fma(z, z, zz);
-        xx = fma(xv, xv, xx);
-    }
-    if (a.npart == nullptr) return;  // uniform across the block
-    t = block_sum(t, sm);
-    zz = block_sum(zz, sm);
-    xx = block_sum(xx, sm);
-    if (threadIdx.x == 0) {
-        a.npart[blockIdx.x] = t;
-        a.npart[a.ntiles + blockIdx.x] = zz;
-        a.npart[2 * a.ntiles + blockIdx.x] = xx;
-    }
-}
-
-// Status block: int32 fail column at [0], double fail value at byte 8,
-// int32 flags[n] at byte 16.
-__device__ __forceinline__ void norm_finish_dev(int64_t i, double t, double zz, double xx,
-                                                double *rii, int32_t *status) {
-    if (!(t > 0.0) || !isfinite(t)) {
-        if (status[0] < 0) {
-            status[0] = (int32_t)i;
-            *reinterpret_cast<double *>(status + 2) = t;
-        }
-        return;
-    }
-    const double unit_roundoff = 1.1102230246251565e-16;  // 2**-53, gram_schmidt.py:33
-    const double nz = sqrt(zz), nx = sqrt(xx);
-    if (t < 100.0 * unit_roundoff * nz * nx) status[4 + i] = 1;  // gram_schmidt.py:155-158
-    *rii = sqrt(t);
-}
-
-// 3 fixed-order sums of the norm partials; optionally finish in place.
-__global__ void __launch_bounds__(kBlock)
-    norm_reduce_kernel(const double *npart, int32_t ntiles, double *tot, int64_t i, double *rii,
-                       int32_t *status) {
-    if (failed(status)) return;
-    __shared__ double sm[kWarps];
-    double v[3];
+    } else {  // ---------------- consumer warps (256 threads) ----------------
+        uint32_t it = 0;
+        RunWalker wk(units, tcols, a.reverse != 0);
+        int64_t tile, cur_tile = -1;
+        int c0, c1;
+        double q[kTmaRpt], p[kTmaRpt], pp[kTmaRpt];
+        while (wk.next(tile, c0, c1)) {
+            const int64_t row0 = tile * kTmaTileRows + threadIdx.x;
+            if (tile != cur_tile) {  // the unit holding column jbeg stores q_i / p_i
+                const bool owner = (t == 0) || (a.reverse ? c0 == 0 : c0 == 0);
+                trail_vectors<kTmaRpt, HP>(a, row0, owner, q, p, pp);
+                cur_tile = tile;
+            } else if (c0 == 0) {
+                trail_vectors<kTmaRpt, HP>(a, row0, true, q, p, pp);
+            }
+            if (t == 0) continue;
+            const bool tma = tile < full_tiles;
+            for (int cc = 0; cc < c1 - c0; ++cc) {
+                const int jr = a.reverse ? c1 - 1 - cc : c0 + cc;  // column relative to jbeg
+                const int j = a.jbeg + jr;
+                const double rj = rsm[jr];
+                double z[kTmaRpt], x[kTmaRpt], d[kTmaRpt];
+                if (tma) {
+                    const int s = it % C::kStages;
+                    const uint32_t ph = (it / C::kStages) & 1;
+                    mbar_wait(full + s, ph);
+                    const double *src = stage_buf + (size_t)s * (C::kStageBytes / 8);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        double s = 0.0;
-        for (int t = threadIdx.x; t < ntiles; t += kBlock) s = __dadd_rn(s, npart[k * ntiles + t]);
-        v[k] = block_sum(s, sm);
-    }
-    if (threadIdx.x == 0) {
-        if (tot) {
-            tot[0] = v[0];
-            tot[1] = v[1];
-            tot[2] = v[2];
+                    for (int u = 0; u < kTmaRpt; ++u) {
+                        z[u] = src[threadIdx.x + u * kBlock];
+                        if (HP) x[u] = src[kTmaTileRows + threadIdx.x + u * kBlock];
+                        if (CGS) d[u] = src[(C::kArrays - 1) * kTmaTileRows + threadIdx.x + u * kBlock];
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + s);
+                    ++it;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kTmaRpt; ++u) {
+                        const int64_t r = row0 + (int64_t)u * kBlock;
+                        const bool ok = r < a.m;
+                        z[u] = ok ? a.W[(int64_t)j * a.ldw + r] : 0.0;
+                        if (HP) x[u] = ok ? a.X[(int64_t)j * a.ldx + r] : 0.0;
+                        if (CGS) d[u] = ok ? a.Z0[(int64_t)j * a.ldz0 + r] : 0.0;
+                    }
+                }
+                double acc = 0.0;
+#pragma unroll
+                for (int u = 0; u < kTmaRpt; ++u) {
+                    const int64_t r = row0 + (int64_t)u * kBlock;
+                    const bool ok = r < a.m;
+                    if (upd) {
+                        z[u] = __dsub_rn(z[u], __dmul_rn(rj, q[u]));
+                        if (ok) __stcs(a.W + (int64_t)j * a.ldw + r, z[u]);
+                        if (HP) {
+                            x[u] = __dsub_rn(x[u], __dmul_rn(rj, pp[u]));
+                            if (ok) __stcs(a.X + (int64_t)j * a.ldx + r, x[u]);
+                        }
+                    }
+                    acc = fma(p[u], CGS ? d[u] : z[u], acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) wsum[warp * kTmaMaxCols + jr] = acc;
+            }
+            consumer_bar();
+            for (int c = c0 + threadIdx.x; c < c1; c += kBlock) {
+                double s = wsum[c];
+#pragma unroll
+                for (int ww = 1; ww < kWarps; ++ww) s = __dadd_rn(s, wsum[ww * kTmaMaxCols + c]);
+                a.partial[(int64_t)c * a.ntiles + tile] = s;
+            }
+            consumer_bar();
         }
-        if (rii) norm_finish_dev(i, v[0], v[1], v[2], rii, status);
+        // ---- r row totals: the last min(t, grid) CTAs to finish reduce ----
+        if (a.counters != nullptr && t > 0) {
+            const unsigned G = gridDim.x;
+            const unsigned K = min((unsigned)t, G);
+            __threadfence();
+            consumer_bar();
+            if (threadIdx.x == 0) s_ticket = atomicAdd(a.counters, 1u);
+            consumer_bar();
+            const unsigned ticket = s_ticket;
+            if (ticket >= G - K) {
+                if (threadIdx.x == 0)
+                    while (*(volatile unsigned *)a.counters < G) __nanosleep(64);
+                consumer_bar();
+                __threadfence();
+                const int r = (int)(ticket - (G - K));
+                for (int c = r; c < t; c += (int)K)
+                    block_totals<1>(a.partial + (int64_t)c * a.ntiles, a.ntiles, a.ntiles, a.rout + c,
+                                    wsum, ConsumerBar());
+                __threadfence();
+                consumer_bar();
+                if (threadIdx.x == 0 && atomicAdd(a.counters + 1, 1u) == K - 1) {
+                    a.counters[0] = 0u;  // every CTA has passed its ticket: reset for the next launch
+                    a.counters[1] = 0u;
+                }
+            }
+        }
     }
 }
-
-__global__ void norm_finish_kernel(int64_t i, const double *tot, double *rii, int32_t *status) {
-    if (failed(status)) return;
-    norm_finish_dev(i, tot[0], tot[1], tot[2], rii, status);
-}
-
-// q = z / rii ; p = x / rii  (normalize(j), gram_schmidt.py:159-165)
-__global__ void __launch_bounds__(kBlock)
-    normalize_kernel(int64_t m, const double *z, const double *rii, double *q, const double *x,
-                     double *p, const int32_t *status) {
-    if (failed(status)) return;
-    const double r = *rii;
-    for (int64_t i = blockIdx.x * (int64_t)kBlock + threadIdx.x; i < m;
-         i += (int64_t)gridDim.x * kBlock) {
-        q[i] = z[i] / r;
-        if (p) p[i] = x[i] / r;
-    }
-}
-
-__global__ void finalize_r_kernel(int64_t n, const double *Rt, double *R, int64_t ldr) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= n * n) return;
-    const int64_t i = idx % n, j = idx / n;  // R column-major: (i, j)
-    R[i + j * ldr] = i <= j ? Rt[i * n + j] : 0.0;
-}
-
-__global__ void status_init_kernel(int32_t *status, int64_t n) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx == 0) {
-        status[0] = -1;
-        status[1] = 0;
-        *reinterpret_cast<double *>(status + 2) = 0.0;
-    }
-    if (idx < n) status[4 + idx] = 0;
-}
-
 // ---------------------------------------------------------------------------
 // Reference kernel namespace (backend.kernels()): dot, sub_scaled, div_scalar
 // ---------------------------------------------------------------------------
@@ -343,90 +765,210 @@ __global__ void div_scalar_kernel(int64_t m, const double *x, const double *r, d
 }
 
 // ---------------------------------------------------------------------------
-// Operators: CSR SpMV / SpMM, dense GEMV / GEMM -- reference-exact order
+// CSR operator: thread-per-row SpMV / SpMM, reference-exact (stored order)
 // ---------------------------------------------------------------------------
+// One thread owns one row.  Its nonzeros are taken in batches of 8: the 8
+// (index, value) loads are issued together, then the 8 gathers of x, then
+// the 8 products are added in stored order with separate rounding, which is
+// bitwise equal to csr_matvec (_kernels_impl.py:50-56).  No shared memory
+// and no barriers on the product path: warps are independent, so the SM
+// keeps ~16 loads per thread in flight across all resident warps (the
+// operator is latency-bound, not bandwidth-bound, at stencil row lengths;
+// consecutive rows share cache lines, so DRAM traffic stays ~1x).  For k > 1
+// (SpMM, the HP block apply) rows of <= 8 nonzeros keep them in registers
+// across all k columns.  The fused variant (HA/naive step, k = 1) gathers x
+// as z - r q (the deferred projection of the previous step, elementwise
+// identical to the separate update), writes the updated z and x = A z, and
+// emits the canonical 256-row norm partials; grid-stride over 256-row
+// blocks, one completion ticket per CTA.
+constexpr int kRowBatch = 8;
 
-// L lanes per row.  Products are formed in parallel, then summed strictly in
-// stored order (shuffle chain), bitwise equal to csr_matvec
-// (_kernels_impl.py:50-56).  k columns handled in one pass (SpMM, the HP
-// block apply) with the row's entries kept in registers.
-template <int L>
-__global__ void __launch_bounds__(kBlock)
-    csr_spmm_kernel(int64_t m, int64_t k, const int32_t *__restrict__ indptr,
-                    const int32_t *__restrict__ indices, const double *__restrict__ data,
-                    const double *__restrict__ X, int64_t ldx, double *__restrict__ Y,
-                    int64_t ldy) {
-    const int64_t gid = blockIdx.x * (int64_t)kBlock + threadIdx.x;
-    const int64_t row = gid / L;
-    if (row >= m) return;  // whole groups exit together
-    const int lane = threadIdx.x & (L - 1);
-    const unsigned mask =
-        L == 32 ? 0xffffffffu : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
-    const int s = __ldg(indptr + row), e = __ldg(indptr + row + 1);
-    if (L == 1) {
-        for (int64_t c = 0; c < k; ++c) {
-            const double *x = X + c * ldx;
-            double acc = 0.0;
-            for (int q = s; q < e; ++q) acc = __dadd_rn(acc, __dmul_rn(__ldg(data + q), __ldg(x + __ldg(indices + q))));
-            Y[row + c * ldy] = acc;
+struct CsrArgs {
+    int64_t m, k;
+    const int32_t *indptr;
+    const int32_t *indices;
+    const double *data;
+    const double *X;
+    int64_t ldx;
+    double *Y;
+    int64_t ldy;
+    // fused step (k == 1)
+    const double *qprev;
+    const double *r;  // r_{i-1,i}; nullptr: gather X as is
+    double *znew;     // updated z_i (own rows)
+    NormOut out;      // out.npart == nullptr: plain apply
+};
+
+// sum_q data[q] * xe(indices[q]) over q in [s, e), xe = x - rj qprev (upd)
+__device__ __forceinline__ double csr_row(const CsrArgs &a, const double *x, int s, int e,
+                                          bool upd, double rj) {
+    double acc = 0.0;
+    for (int q0 = s; q0 < e; q0 += kRowBatch) {
+        int c[kRowBatch];
+        double v[kRowBatch], xv[kRowBatch];
+#pragma unroll
+        for (int h = 0; h < kRowBatch; ++h) {
+            const bool ok = q0 + h < e;
+            c[h] = ok ? __ldg(a.indices + q0 + h) : 0;
+            v[h] = ok ? __ldg(a.data + q0 + h) : 0.0;
         }
+#pragma unroll
+        for (int h = 0; h < kRowBatch; ++h) {
+            xv[h] = q0 + h < e ? __ldg(x + c[h]) : 0.0;
+            if (upd && q0 + h < e) xv[h] = __dsub_rn(xv[h], __dmul_rn(rj, __ldg(a.qprev + c[h])));
+        }
+#pragma unroll
+        for (int h = 0; h < kRowBatch; ++h)
+            if (q0 + h < e) acc = __dadd_rn(acc, __dmul_rn(v[h], xv[h]));
+    }
+    return acc;
+}
+
+// R rows at once: when every row has <= kRowBatch nonzeros, all R rows'
+// (index, value) loads are issued together, then all R x R gathers, then the
+// sums in stored order; otherwise row by row (csr_row).  Same arithmetic.
+template <int R>
+__device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], const int (&e)[R],
+                                         bool upd, double rj, double (&y)[R]) {
+    bool short_rows = true;
+#pragma unroll
+    for (int i = 0; i < R; ++i) short_rows &= (e[i] - s[i] <= kRowBatch);
+    if (!short_rows) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) y[i] = csr_row(a, a.X, s[i], e[i], upd, rj);
         return;
     }
-    if (e - s <= L) {
-        const int q = s + lane;
-        const bool has = q < e;
-        const double v = has ? __ldg(data + q) : 0.0;
-        const int col = has ? __ldg(indices + q) : 0;
-        const int cnt = e - s;
-        for (int64_t c = 0; c < k; ++c) {
-            const double prod = has ? __dmul_rn(v, __ldg(X + c * ldx + col)) : 0.0;
-            double acc = 0.0;
-            for (int u = 0; u < cnt; ++u) acc = __dadd_rn(acc, __shfl_sync(mask, prod, u, L));
-            if (lane == 0) Y[row + c * ldy] = acc;
+    int c[R][kRowBatch];
+    double v[R][kRowBatch], xv[R][kRowBatch];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int h = 0; h < kRowBatch; ++h) {
+            const bool ok = s[i] + h < e[i];
+            c[i][h] = ok ? __ldg(a.indices + s[i] + h) : 0;
+            v[i][h] = ok ? __ldg(a.data + s[i] + h) : 0.0;
         }
-    } else {
-        for (int64_t c = 0; c < k; ++c) {
-            const double *x = X + c * ldx;
-            double acc = 0.0;
-            for (int base = s; base < e; base += L) {
-                const int q = base + lane;
-                const double prod = q < e ? __dmul_rn(__ldg(data + q), __ldg(x + __ldg(indices + q))) : 0.0;
-                const int cnt = min(L, e - base);
-                for (int u = 0; u < cnt; ++u) acc = __dadd_rn(acc, __shfl_sync(mask, prod, u, L));
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int h = 0; h < kRowBatch; ++h) {
+            const bool ok = s[i] + h < e[i];
+            xv[i][h] = ok ? __ldg(a.X + c[i][h]) : 0.0;
+            if (upd && ok) xv[i][h] = __dsub_rn(xv[i][h], __dmul_rn(rj, __ldg(a.qprev + c[i][h])));
+        }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int h = 0; h < kRowBatch; ++h)
+            if (s[i] + h < e[i]) acc = __dadd_rn(acc, __dmul_rn(v[i][h], xv[i][h]));
+        y[i] = acc;
+    }
+}
+
+// Plain apply, k >= 1 columns: grid-stride over 256-row blocks.
+__global__ void __launch_bounds__(kBlock) csr_row_kernel(CsrArgs a) {
+    const int64_t nblocks = (a.m + kBlock - 1) / kBlock;
+    for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+        const int64_t row = blk * kBlock + threadIdx.x;
+        if (row >= a.m) continue;
+        const int s = __ldg(a.indptr + row);
+        const int e = __ldg(a.indptr + row + 1);
+        if (e - s <= kRowBatch && a.k > 1) {  // entries stay in registers across columns
+            int c[kRowBatch];
+            double val[kRowBatch];
+#pragma unroll
+            for (int h = 0; h < kRowBatch; ++h) {
+                const bool ok = s + h < e;
+                c[h] = ok ? __ldg(a.indices + s + h) : 0;
+                val[h] = ok ? __ldg(a.data + s + h) : 0.0;
             }
-            if (lane == 0) Y[row + c * ldy] = acc;
+            for (int64_t col = 0; col < a.k; ++col) {
+                const double *x = a.X + col * a.ldx;
+                double xv[kRowBatch];
+#pragma unroll
+                for (int h = 0; h < kRowBatch; ++h) xv[h] = s + h < e ? __ldg(x + c[h]) : 0.0;
+                double acc = 0.0;
+#pragma unroll
+                for (int h = 0; h < kRowBatch; ++h)
+                    if (s + h < e) acc = __dadd_rn(acc, __dmul_rn(val[h], xv[h]));
+                a.Y[row + col * a.ldy] = acc;
+            }
+        } else {
+            for (int64_t col = 0; col < a.k; ++col)
+                a.Y[row + col * a.ldy] = csr_row(a, a.X + col * a.ldx, s, e, false, 0.0);
         }
     }
 }
 
-// Dense y = A x, one thread per row, ascending j, separately rounded
-// (bitwise equal to matvec, _kernels_impl.py:24-32).  Loads of A are
-// coalesced across the warp (column-major); 16 in flight per thread.
+// Fused HA/naive step: grid-stride over the 256-row norm tiles, one row per
+// thread, one barrier pair per tile, one completion ticket per CTA.
+__global__ void __launch_bounds__(kBlock) csr_step_kernel(CsrArgs a) {
+    if (failed(a.out.status)) return;
+    __shared__ double sm[3 * kWarps];
+    const bool upd = a.r != nullptr;
+    const double rj = upd ? *a.r : 0.0;
+    const int64_t ntiles = (a.m + kBlock - 1) / kBlock;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row = tile * kBlock + threadIdx.x;
+        const bool ok = row < a.m;
+        int s[1], e[1];
+        double y[1];
+        s[0] = ok ? __ldg(a.indptr + row) : 0;
+        e[0] = ok ? __ldg(a.indptr + row + 1) : 0;
+        csr_rows<1>(a, s, e, upd, rj, y);
+        double z = 0.0;
+        if (ok) {
+            z = a.X[row];
+            if (upd) z = __dsub_rn(z, __dmul_rn(rj, a.qprev[row]));
+            a.Y[row] = y[0];
+            if (a.znew) a.znew[row] = z;
+        }
+        norm_sub_partial(0, ok ? fma(z, y[0], 0.0) : 0.0, ok ? fma(z, z, 0.0) : 0.0,
+                         ok ? fma(y[0], y[0], 0.0) : 0.0, sm);
+        norm_tiles_finish<1>(a.out, tile, sm);
+    }
+    norm_last_cta(a.out);
+}
+
+// ---------------------------------------------------------------------------
+// Dense operator: GEMV / GEMM, reference-exact (ascending column index)
+// ---------------------------------------------------------------------------
+// y = A x, one thread per row, ascending j, separately rounded (bitwise equal
+// to matvec, _kernels_impl.py:24-32).  Loads of A are coalesced across the
+// warp (column-major); x is staged in shared memory in chunks.
 constexpr int kGemvBlock = 128;
+constexpr int kGemvChunk = 2048;
 __global__ void __launch_bounds__(kGemvBlock)
     dense_gemv_kernel(int64_t m, const double *__restrict__ A, int64_t lda,
                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y,
                       int64_t ldy) {
+    __shared__ double xs[kGemvChunk];
     const int64_t row = blockIdx.x * (int64_t)kGemvBlock + threadIdx.x;
     const double *x = X + blockIdx.y * ldx;
-    if (row >= m) return;
-    const double *a = A + row;
+    const double *arow = A + min(row, m - 1);
     double acc = 0.0;
-    int64_t j = 0;
     constexpr int U = 16;
-    for (; j + U <= m; j += U) {
-        double av[U];
+    for (int64_t j0 = 0; j0 < m; j0 += kGemvChunk) {
+        const int len = (m - j0) < kGemvChunk ? (int)(m - j0) : kGemvChunk;
+        __syncthreads();
+        for (int q = threadIdx.x; q < len; q += kGemvBlock) xs[q] = __ldg(x + j0 + q);
+        __syncthreads();
+        int j = 0;
+        for (; j + U <= len; j += U) {
+            double av[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) av[u] = __ldg(a + (j + u) * lda);
+            for (int u = 0; u < U; ++u) av[u] = __ldg(arow + (j0 + j + u) * lda);
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(av[u], __ldg(x + j + u)));
+            for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(av[u], xs[j + u]));
+        }
+        for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(arow + (j0 + j) * lda), xs[j]));
     }
-    for (; j < m; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(a + j * lda), __ldg(x + j)));
-    Y[row + blockIdx.y * ldy] = acc;
+    if (row < m) Y[row + blockIdx.y * ldy] = acc;
 }
 
-// Dense Y = A X (k columns), shared-memory tiled, every output accumulated
-// over ascending j with separate rounding: bitwise equal to k matvecs
+// Y = A X (k columns), shared-memory tiled, every output accumulated over
+// ascending j with separate rounding: bitwise equal to k matvecs
 // (apply_block_dense, _kernels_impl.py:35-47).
 constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
 __global__ void __launch_bounds__(256)
