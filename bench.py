@@ -197,7 +197,7 @@ def run_b200(args, rank, world, local_rank):
     from paper_1703_10440_b200 import _lib
 
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    if world > 1 or os.environ.get("AQR_BENCH_DIST"):
         return run_b200_distributed(args, rank, world, local_rank)
     L = _lib.lib()
     family, variant, orientation = args.method.split("-")
@@ -313,7 +313,81 @@ def run_b200(args, rank, world, local_rank):
 
 
 def run_b200_distributed(args, rank, world, local_rank):
-    raise NotImplementedError("multi-GPU bench path not wired yet")
+    """N > 1: config 2 row-partitioned over N GPUs (strong scaling), NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1703_10440_b200 import _lib
+    from paper_1703_10440_b200 import distributed as DD
+
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local_rank))
+    L = _lib.lib()
+    indptr, indices, data, Z = workload()
+    m, n = Z.shape
+    part = DD.row_partition(m, world, align=M_SIDE)  # whole grid rows per rank
+    r0, r1 = part[rank]
+    op = DD.DistCsrSpdOperator(indptr[r0:r1 + 1] - indptr[r0], indices[indptr[r0]:indptr[r1]],
+                               data[indptr[r0]:indptr[r1]], part, rank)
+    Zd = torch.from_numpy(np.ascontiguousarray(Z[r0:r1].T)).cuda().t()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        DD.dist_factorize(Zd, op, args.method)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.aqr_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            DD.dist_factorize(Zd, op, args.method)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    launches = int(L.aqr_launch_count() - launches0)
+    ms_per_step = ms / args.steps
+    value = n * args.steps / (ms / 1e3)
+    # end to end: pinned host row block in, host Q block + R out, every rank
+    e2e = None
+    if not args.no_e2e:
+        Zh = torch.empty((n, r1 - r0), dtype=torch.float64).pin_memory().t()
+        Zh.copy_(torch.from_numpy(Z[r0:r1]))
+        Qh = torch.empty((n, r1 - r0), dtype=torch.float64).pin_memory().t()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = DD.dist_factorize(Zh.to("cuda", non_blocking=True), op, args.method)
+            Qh.copy_(res.Q, non_blocking=True)
+            Rh = res.R.cpu()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * m * n, "d2h_bytes_per_step": 8 * m * n + 8 * n * n * world}
+        del Rh
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded 5-pt Laplacian + N(0,1) Z; no dataset named by the reference)",
+            "config": {"workload": "config2 row-partitioned: 5-pt Laplacian 1024^2 + 1e-2 I (CSR), "
+                                   "Z 1048576x64 N(0,1)", "method": args.method, "m": m, "n": n,
+                       "parallelism": f"rows/{world} (NCCL all-reduce per step, SpMV halo exchange)",
+                       "l2": "inputs larger than L2, no flush"},
+            "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+            "roofline": None, "cpu_baseline": None, "e2e": e2e, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def main():

@@ -89,6 +89,9 @@ typedef struct aqr_op {
     aqr_apply_fn apply;       /* called with k == 1                      */
     aqr_apply_fn apply_block; /* called with k == n (HP); may equal apply */
     void *ctx;
+    /* AQR_OP_DENSE: columns of A (0 = m, square).  A local row panel of a
+     * row-partitioned operator is m_local x ncols (multi-GPU driver). */
+    int64_t ncols;
 } aqr_op;
 
 /* Everything _gs_factor takes and returns.  Inputs above the marker. */

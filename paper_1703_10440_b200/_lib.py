@@ -40,6 +40,7 @@ class AqrOp(ctypes.Structure):
         ("A", c_vp), ("lda", c_i64),
         ("indptr", c_vp), ("indices", c_vp), ("data", c_vp), ("nnz", c_i64),
         ("apply", APPLY_FN), ("apply_block", APPLY_FN), ("ctx", c_vp),
+        ("ncols", c_i64),
     ]
 
 

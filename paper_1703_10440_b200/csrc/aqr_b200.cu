@@ -193,15 +193,16 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
 aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                        int64_t ldy, cudaStream_t s) {
     const int64_t m = op->m;
+    const int64_t ncols = op->ncols > 0 ? op->ncols : m;
     if (m == 0) return AQR_OK;
     if (k == 1) {
         dim3 grid((unsigned)((m + aqr::kGemvBlock - 1) / aqr::kGemvBlock), 1);
-        aqr::dense_gemv_kernel<<<grid, aqr::kGemvBlock, 0, s>>>(m, op->A, op->lda, X, ldx, Y, ldy);
+        aqr::dense_gemv_kernel<<<grid, aqr::kGemvBlock, 0, s>>>(m, ncols, op->A, op->lda, X, ldx, Y, ldy);
         return launched("dense_gemv_kernel");
     }
     dim3 grid((unsigned)((m + aqr::kGemmBM - 1) / aqr::kGemmBM),
               (unsigned)((k + aqr::kGemmBN - 1) / aqr::kGemmBN));
-    aqr::dense_gemm_kernel<<<grid, 256, 0, s>>>(m, k, op->A, op->lda, X, ldx, Y, ldy);
+    aqr::dense_gemm_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
     return launched("dense_gemm_kernel");
 }
 
@@ -790,7 +791,8 @@ aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientati
 
 aqr_status aqr_op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                         int64_t ldy, void *stream) {
-    if (!op || k < 0 || ldx < op->m || ldy < op->m) return set_err(AQR_EARG, "bad apply arguments");
+    const int64_t xrows = (op && op->kind == AQR_OP_DENSE && op->ncols > 0) ? op->ncols : (op ? op->m : 0);
+    if (!op || k < 0 || (k > 1 && ldx < xrows) || ldy < op->m) return set_err(AQR_EARG, "bad apply arguments");
     if (k == 0) return AQR_OK;
     return op_apply(op, k, X, ldx, Y, ldy, S(stream));
 }

@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(kBlock) csr_step_kernel(CsrArgs a) {
 constexpr int kGemvBlock = 128;
 constexpr int kGemvChunk = 2048;
 __global__ void __launch_bounds__(kGemvBlock)
-    dense_gemv_kernel(int64_t m, const double *__restrict__ A, int64_t lda,
+    dense_gemv_kernel(int64_t m, int64_t ncols, const double *__restrict__ A, int64_t lda,
                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y,
                       int64_t ldy) {
     __shared__ double xs[kGemvChunk];
@@ -949,8 +949,8 @@ __global__ void __launch_bounds__(kGemvBlock)
     const double *arow = A + min(row, m - 1);
     double acc = 0.0;
     constexpr int U = 16;
-    for (int64_t j0 = 0; j0 < m; j0 += kGemvChunk) {
-        const int len = (m - j0) < kGemvChunk ? (int)(m - j0) : kGemvChunk;
+    for (int64_t j0 = 0; j0 < ncols; j0 += kGemvChunk) {
+        const int len = (ncols - j0) < kGemvChunk ? (int)(ncols - j0) : kGemvChunk;
         __syncthreads();
         for (int q = threadIdx.x; q < len; q += kGemvBlock) xs[q] = __ldg(x + j0 + q);
         __syncthreads();
@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(kGemvBlock)
 // (apply_block_dense, _kernels_impl.py:35-47).
 constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
 __global__ void __launch_bounds__(256)
-    dense_gemm_kernel(int64_t m, int64_t k, const double *__restrict__ A, int64_t lda,
+    dense_gemm_kernel(int64_t m, int64_t ncols, int64_t k, const double *__restrict__ A, int64_t lda,
                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y,
                       int64_t ldy) {
     __shared__ double As[kGemmBK][kGemmBM + 1];
@@ -984,19 +984,19 @@ __global__ void __launch_bounds__(256)
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    for (int64_t j0 = 0; j0 < m; j0 += kGemmBK) {
+    for (int64_t j0 = 0; j0 < ncols; j0 += kGemmBK) {
         for (int e = threadIdx.x; e < kGemmBM * kGemmBK; e += 256) {
             const int ii = e % kGemmBM, jj = e / kGemmBM;
             const int64_t gi = i0 + ii, gj = j0 + jj;
-            As[jj][ii] = (gi < m && gj < m) ? A[gi + gj * lda] : 0.0;
+            As[jj][ii] = (gi < m && gj < ncols) ? A[gi + gj * lda] : 0.0;
         }
         for (int e = threadIdx.x; e < kGemmBN * kGemmBK; e += 256) {
             const int jj = e % kGemmBK, cc = e / kGemmBK;
             const int64_t gj = j0 + jj, gc = c0 + cc;
-            Xs[jj][cc] = (gj < m && gc < k) ? X[gj + gc * ldx] : 0.0;
+            Xs[jj][cc] = (gj < ncols && gc < k) ? X[gj + gc * ldx] : 0.0;
         }
         __syncthreads();
-        const int kmax = (m - j0) < kGemmBK ? (int)(m - j0) : kGemmBK;
+        const int kmax = (ncols - j0) < kGemmBK ? (int)(ncols - j0) : kGemmBK;
         for (int jj = 0; jj < kmax; ++jj) {
             double av[4], xv[4];
 #pragma unroll

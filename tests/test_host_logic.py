@@ -108,7 +108,7 @@ def test_c_abi_library_exports_every_header_symbol():
 
 def test_ctypes_struct_layout_matches_header():
     # aqr_op / aqr_factor_args as declared in include/aqr_b200.h (LP64)
-    assert ctypes.sizeof(_lib.AqrOp) == 4 + 4 + 8 + 8 + 8 + 8 * 3 + 8 + 8 * 3
+    assert ctypes.sizeof(_lib.AqrOp) == 4 + 4 + 8 + 8 + 8 + 8 * 3 + 8 + 8 * 3 + 8
     assert _lib.AqrFactorArgs.flagged_host.offset == 4 * 4 + 8 * 2 + 8 * 6 + 8 + 8 + 8 + 8 + 8 + 8
 
 
