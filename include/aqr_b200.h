@@ -224,6 +224,9 @@ AQR_API aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double
 /* Same for any timed kernel slot (0 trailing, 1 fused SpMV step, 2 column
  * update + norm), without resetting; enabling the timer resets it. */
 AQR_API aqr_status aqr_kernel_timer_read(int32_t slot, int64_t *launches, double *ms, double *bytes);
+/* Per-launch device times (ms) and algorithmic bytes of a slot, in launch
+ * order; returns the number of timed launches (-1 on a CUDA error). */
+AQR_API int64_t aqr_kernel_timer_list(int32_t slot, double *ms_out, double *bytes_out, int64_t max);
 
 AQR_API const char *aqr_last_error(void);
 AQR_API int32_t aqr_abi_version(void);

@@ -89,6 +89,7 @@ SIGNATURES = {
                                         ctypes.POINTER(c_dbl)]),
     "aqr_kernel_timer_read": (c_i32, [c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl),
                                       ctypes.POINTER(c_dbl)]),
+    "aqr_kernel_timer_list": (c_i64, [c_i32, c_vp, c_vp, c_i64]),
     "aqr_last_error": (ctypes.c_char_p, []),
     "aqr_abi_version": (c_i32, []),
 }

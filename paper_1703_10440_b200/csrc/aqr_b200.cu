@@ -148,6 +148,59 @@ int trail_variant() {
     return v;
 }
 
+// Experiment knob (read once): AQR_CARVEOUT = -1 leaves the driver's choice,
+// otherwise the preferred shared-memory carveout (percent) of the per-step
+// kernels, so consecutive launches need no L1/shared reconfiguration.
+int carveout_pct() {
+    static const int v = [] {
+        const char *e = std::getenv("AQR_CARVEOUT");
+        return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
+template <typename K>
+void ensure_carveout(K kernel) {
+    const int pct = carveout_pct();
+    if (pct < 0) return;
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void *key = reinterpret_cast<const void *>(kernel);
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &e : done)
+        if (e.first == key && e.second == dev) return;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    done.push_back({key, dev});
+}
+
+// Programmatic dependent launch for the per-step kernels (AQR_PDL=0 disables).
+int pdl_mode() {
+    static const int v = [] {
+        const char *e = std::getenv("AQR_PDL");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args) {
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_mode() != 0 ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ---- operators ---------------------------------------------------------------
 
 aqr::NormOut no_norm() {
@@ -181,8 +234,20 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
     if (out.npart != nullptr) {
         const int64_t nt = aqr::norm_tiles(op->m);
         const long tix = timer_begin(1, (double)op->m * 40.0 + (double)op->nnz * 12.0, s);
-        aqr::csr_step_kernel<<<(unsigned)std::min<int64_t>(nt, (int64_t)sm_count() * 8), aqr::kBlock, 0,
-                                  s>>>(a);
+        static const int sv = [] {
+            const char *e = std::getenv("AQR_SPMV_VARIANT");
+            return e ? std::atoi(e) : 0;
+        }();
+        const unsigned g1 = (unsigned)nt;  // the canonical norm grid
+        ensure_carveout(aqr::csr_step_kernel<8, 4>);
+        ensure_carveout(aqr::csr_step_kernel<6, 6>);
+        ensure_carveout(aqr::csr_step_kernel<8, 1>);
+        if (sv == 0)
+            launch_pdl(aqr::csr_step_kernel<8, 4>, g1, aqr::kBlock, 0, s, a);
+        else if (sv == 1)
+            launch_pdl(aqr::csr_step_kernel<6, 6>, g1, aqr::kBlock, 0, s, a);
+        else
+            launch_pdl(aqr::csr_step_kernel<8, 1>, g1, aqr::kBlock, 0, s, a);
         timer_end(tix, s);
         return launched("csr_step_kernel");
     }
@@ -252,10 +317,11 @@ aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, dou
     a.out.ntiles = (int32_t)aqr::norm_tiles(m);
     const int64_t nt = aqr::norm_tiles(m);
     if (nt == 0) return AQR_OK;
-    const int64_t grid = std::min<int64_t>(nt, (int64_t)sm_count() * 8);
+    const int64_t grid = nt;  // the canonical norm grid (also without norm output)
+    ensure_carveout(aqr::col_update_norm_kernel);
     const long tix = timer_begin(2, (double)m * (8.0 + (r ? 16.0 : 0.0) + (x ? (r ? 24.0 : 8.0) : 0.0) +
                                                  (xnorm ? 8.0 : 0.0)), s);
-    aqr::col_update_norm_kernel<<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    launch_pdl(aqr::col_update_norm_kernel, (unsigned)grid, aqr::kBlock, 0, s, a);
     timer_end(tix, s);
     return launched("col_update_norm_kernel");
 }
@@ -306,6 +372,8 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     do {                                                                                         \
         constexpr size_t smem = aqr::TmaCfg<HP, CGS>::kSmem;                                     \
         AQR_TRY(ensure_smem(aqr::trailing_tma_kernel<HP, CGS, true>, smem));                     \
+        ensure_carveout(aqr::trailing_tma_kernel<HP, CGS, true>);                                \
+        ensure_carveout(aqr::trailing_tma_kernel<HP, CGS, false>);                               \
         AQR_TRY(ensure_smem(aqr::trailing_tma_kernel<HP, CGS, false>, smem));                    \
         /* all CTAs must be co-resident: the last ones wait for the grid */                     \
         static int occ[64] = {0};                                                                \
@@ -319,9 +387,9 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
         }                                                                                        \
         const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sm_count() * occ[dev_ & 63]); \
         if (trail_variant() == 1)                                                                \
-            aqr::trailing_tma_kernel<HP, CGS, false><<<grid, aqr::kTmaThreads, smem, s>>>(a);    \
+            launch_pdl(aqr::trailing_tma_kernel<HP, CGS, false>, grid, aqr::kTmaThreads, smem, s, a); \
         else                                                                                     \
-            aqr::trailing_tma_kernel<HP, CGS, true><<<grid, aqr::kTmaThreads, smem, s>>>(a);     \
+            launch_pdl(aqr::trailing_tma_kernel<HP, CGS, true>, grid, aqr::kTmaThreads, smem, s, a); \
     } while (0)
         if (hp) { if (cgs) TMA_LAUNCH(true, true); else TMA_LAUNCH(true, false); }
         else    { if (cgs) TMA_LAUNCH(false, true); else TMA_LAUNCH(false, false); }
@@ -332,7 +400,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
 #define LAUNCH(RPT, CU, HP, CGS)                                                   \
     do {                                                                           \
         AQR_TRY(ensure_smem(aqr::trailing_kernel<RPT, CU, HP, CGS>, smem));        \
-        aqr::trailing_kernel<RPT, CU, HP, CGS><<<grid, aqr::kBlock, smem, s>>>(a); \
+        launch_pdl(aqr::trailing_kernel<RPT, CU, HP, CGS>, grid, aqr::kBlock, smem, s, a); \
     } while (0)
         if (big) {
             if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
@@ -364,6 +432,108 @@ aqr_status launch_normalize(int64_t m, const double *z, const double *rii, doubl
     return launched("normalize_kernel");
 }
 
+// ---- side streams for the look-ahead schedule ------------------------------
+struct SideCtx {
+    int dev;
+    cudaStream_t side;
+    cudaEvent_t e1, e2;
+};
+std::mutex g_side_mu;
+std::vector<SideCtx> g_side_free;
+
+aqr_status side_acquire(SideCtx &c) {
+    int dev = 0;
+    AQR_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_side_mu);
+        for (size_t k = 0; k < g_side_free.size(); ++k)
+            if (g_side_free[k].dev == dev) {
+                c = g_side_free[k];
+                g_side_free.erase(g_side_free.begin() + (long)k);
+                return AQR_OK;
+            }
+    }
+    int lo = 0, hi = 0;
+    AQR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    c.dev = dev;
+    AQR_CUDA(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi));
+    AQR_CUDA(cudaEventCreateWithFlags(&c.e1, cudaEventDisableTiming));
+    AQR_CUDA(cudaEventCreateWithFlags(&c.e2, cudaEventDisableTiming));
+    return AQR_OK;
+}
+
+void side_release(const SideCtx &c) {
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    g_side_free.push_back(c);
+}
+
+int lookahead_mode() {  // AQR_LOOKAHEAD=0 disables (A/B experiments)
+    static const int v = [] {
+        const char *e = std::getenv("AQR_LOOKAHEAD");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// ---- L2 residency of the operator --------------------------------------------
+// The CSR operator (values, indices, row pointers: 12 nnz + 4 m bytes, 67 MB
+// at config 2) is re-read by every step's SpMV while the trailing pass
+// streams ~1 GB per step through the 126 MB L2 (with evict-first hints).
+// When the three arrays are adjacent in memory (the Python operator
+// allocates them in one block), a persisting access-policy window on the
+// stream keeps them L2-resident for the whole factorization.
+struct L2Window {
+    bool active = false;
+    cudaStream_t s = nullptr;
+};
+
+int l2_persist_mode() {  // AQR_L2_PERSIST=0 disables (A/B experiments)
+    static const int v = [] {
+        const char *e = std::getenv("AQR_L2_PERSIST");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+aqr_status l2_window_begin(const aqr_op *op, cudaStream_t s, L2Window &w) {
+    if (l2_persist_mode() == 0 || op->kind != AQR_OP_CSR || op->nnz <= 0) return AQR_OK;
+    const uintptr_t p0 = (uintptr_t)op->data, p1 = (uintptr_t)op->indices, p2 = (uintptr_t)op->indptr;
+    const uintptr_t lo = std::min(p0, std::min(p1, p2));
+    const uintptr_t hi = std::max(p0 + 8 * (uintptr_t)op->nnz,
+                                  std::max(p1 + 4 * (uintptr_t)op->nnz, p2 + 4 * (uintptr_t)(op->m + 1)));
+    const size_t need = 12 * (size_t)op->nnz + 4 * (size_t)(op->m + 1);
+    if (hi - lo > need + need / 8) return AQR_OK;  // not one block: leave the cache alone
+    int dev = 0, max_win = 0, max_persist = 0;
+    AQR_CUDA(cudaGetDevice(&dev));
+    AQR_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    AQR_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    if (max_win <= 0 || max_persist <= 0) return AQR_OK;
+    const size_t bytes = std::min<size_t>(hi - lo, (size_t)max_win);
+    const size_t persist = std::min<size_t>(bytes, (size_t)max_persist);
+    AQR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+    cudaStreamAttrValue attr;
+    std::memset(&attr, 0, sizeof attr);
+    attr.accessPolicyWindow.base_ptr = reinterpret_cast<void *>(lo);
+    attr.accessPolicyWindow.num_bytes = bytes;
+    attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)bytes);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    AQR_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
+    w.active = true;
+    w.s = s;
+    return AQR_OK;
+}
+
+void l2_window_end(L2Window &w) {
+    if (!w.active) return;
+    cudaStreamAttrValue attr;
+    std::memset(&attr, 0, sizeof attr);
+    attr.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(w.s, cudaStreamAttributeAccessPolicyWindow, &attr);
+    cudaCtxResetPersistingL2Cache();
+    w.active = false;
+}
+
 // ---- workspace ---------------------------------------------------------------
 
 inline uint64_t al(uint64_t b) { return (b + 255) & ~uint64_t(255); }
@@ -389,8 +559,8 @@ Layout layout(int32_t family, int32_t variant, int32_t orientation, int64_t m, i
     L.rt = take(8 * nn * nn);
     L.partial = take(8 * nn * ntiles);
     L.npart = take(8 * 3 * std::max<uint64_t>((uint64_t)aqr::norm_tiles(m), 1));
-    L.xvec = variant != AQR_HP ? take(8 * mm) : kNone;
-    L.zvec = variant != AQR_HP ? take(8 * mm) : kNone;
+    L.xvec = variant != AQR_HP ? take(8 * 2 * mm) : kNone;  // 2-slot ring (look-ahead)
+    L.zvec = variant != AQR_HP ? take(8 * 2 * mm) : kNone;
     L.pvec = (variant == AQR_NAIVE && orientation == AQR_ROW) ? take(8 * mm) : kNone;
     L.pring = (variant == AQR_HP && orientation == AQR_ROW) ? take(8 * 2 * mm) : kNone;
     L.P = orientation == AQR_COL ? take(8 * mm * nn) : kNone;
@@ -529,6 +699,73 @@ struct Run {
         return AQR_OK;
     }
 
+    // Norm step of column j on stream st (look-ahead schedule): HP updates
+    // z_j, x_j and forms the norm; native CSR HA runs the fused SpMV step
+    // into ring slot j & 1.
+    aqr_status norm_step_la(int64_t j, cudaStream_t st, const double *&zcol, const double *&xcol) {
+        double *z = col(W, ldw, j);
+        const double *qprev = j > 0 ? col(W, ldw, j - 1) : nullptr;
+        const double *r = j > 0 ? rt(j - 1, j) : nullptr;
+        if (hp) {
+            const double *pprev = j > 0 ? pring + ((j - 1) & 1) * m : nullptr;
+            double *x = col(X, m, j);
+            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev, r, nullptr, norm_out(j), st));
+            zcol = z;
+            xcol = x;
+        } else {
+            double *xs = xvec + (j & 1) * m, *zs = zvec + (j & 1) * m;
+            AQR_TRY(launch_csr(a->op, 1, z, m, xs, m, qprev, r, zs, norm_out(j), st));
+            ++mv;
+            zcol = zs;
+            xcol = xs;
+        }
+        return AQR_OK;
+    }
+
+    // Look-ahead row form (native CSR HA, HP).  Step i's trailing pass is
+    // split: T_first updates column i+1 and forms r_{i,i+1} (and stores
+    // q_i, p_i); then the norm step of column i+1 (the latency-bound SpMV
+    // for HA) runs on the side stream concurrently with T_rest, the
+    // bandwidth-bound pass over columns i+2..n-1.  Same kernels, same
+    // per-element operations and reduction trees: bitwise identical to
+    // row_form().
+    aqr_status row_form_lookahead(cudaStream_t side, cudaEvent_t e1, cudaEvent_t e2) {
+        const double *zc = nullptr, *xc = nullptr;
+        AQR_TRY(norm_step_la(0, s, zc, xc));
+        for (int64_t i = 0; i < n; ++i) {
+            const double *pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
+            aqr::TrailArgs t = trail(i, i + 1, std::min<int64_t>(i + 2, n));
+            t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+            t.pprev = pprev;
+            t.reverse = (int32_t)(i & 1);
+            t.psrc = xc;
+            t.rii = rt(i, i);
+            t.zsrc = zc;
+            t.qout = col(W, ldw, i);
+            t.pout = hp ? pring + (i & 1) * m : nullptr;
+            AQR_TRY(launch_trailing(t, hp, cgs, s));  // T_first (vector-only at i = n-1)
+            if (i + 1 >= n) break;
+            AQR_CUDA(cudaEventRecord(e1, s));
+            AQR_CUDA(cudaStreamWaitEvent(side, e1, 0));
+            const double *zn = nullptr, *xn = nullptr;
+            AQR_TRY(norm_step_la(i + 1, side, zn, xn));
+            AQR_CUDA(cudaEventRecord(e2, side));
+            if (i + 2 < n) {  // T_rest: columns i+2.., q_i / p_i already stored
+                aqr::TrailArgs t2 = trail(i, i + 2, n);
+                t2.qprev = t.qprev;
+                t2.pprev = pprev;
+                t2.reverse = t.reverse;
+                t2.psrc = xc;
+                t2.rii = rt(i, i);
+                AQR_TRY(launch_trailing(t2, hp, cgs, s));
+            }
+            AQR_CUDA(cudaStreamWaitEvent(s, e2, 0));
+            zc = zn;
+            xc = xn;
+        }
+        return AQR_OK;
+    }
+
     aqr_status col_form() {
         for (int64_t j = 0; j < n; ++j) {
             for (int64_t i = 0; i < j; ++i) {  // project(i, j), lines 169-170
@@ -587,6 +824,23 @@ aqr_status aqr_kernel_timer_read(int32_t slot, int64_t *launches, double *ms, do
     if (ms) *ms = total;
     if (bytes) *bytes = b;
     return AQR_OK;
+}
+
+int64_t aqr_kernel_timer_list(int32_t slot, double *ms_out, double *bytes_out, int64_t max) {
+    std::lock_guard<std::mutex> lk(g_timer.mu);
+    int64_t k = 0;
+    for (const auto &r : g_timer.recs) {
+        if (r.slot != slot) continue;
+        if (k < max) {
+            if (cudaEventSynchronize(r.e1) != cudaSuccess) return -1;
+            float dt = 0.f;
+            if (cudaEventElapsedTime(&dt, r.e0, r.e1) != cudaSuccess) return -1;
+            if (ms_out) ms_out[k] = dt;
+            if (bytes_out) bytes_out[k] = r.bytes;
+        }
+        ++k;
+    }
+    return k;
 }
 
 aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double *bytes) {
@@ -670,9 +924,22 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
     }
     static const bool debug_timing = std::getenv("AQR_DEBUG_TIMING") != nullptr;
     const auto t_loop = std::chrono::steady_clock::now();
-    AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
+    L2Window l2w;
+    AQR_TRY(l2_window_begin(a->op, s, l2w));
+    const bool lookahead = a->orientation == AQR_ROW && lookahead_mode() != 0 &&
+                           (r.hp || (r.csr_native && a->variant == AQR_HA));
+    if (lookahead) {
+        SideCtx sc;
+        AQR_TRY(side_acquire(sc));
+        const aqr_status st_la = r.row_form_lookahead(sc.side, sc.e1, sc.e2);
+        side_release(sc);
+        AQR_TRY(st_la);
+    } else {
+        AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
+    }
     aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, r.Rt, a->R, a->ldr);
     AQR_TRY(launched("finalize_r_kernel"));
+    l2_window_end(l2w);
     std::vector<int32_t> st((16 + 4 * n) / 4);
     AQR_CUDA(cudaMemcpyAsync(st.data(), r.status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
     const auto t_enq = std::chrono::steady_clock::now();

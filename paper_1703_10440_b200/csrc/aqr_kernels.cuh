@@ -10,7 +10,8 @@
 //     tile owns rows k + 256 u (u = 0..RPT-1), accumulates them in ascending u
 //     with fma, the warp reduces with an xor butterfly (16, 8, 4, 2, 1) and the
 //     8 warps are added in ascending order -> one partial per (tile, column);
-//   * the norm partials (z.x, z.z, x.x) use 256-row tiles (block tree);
+//   * the norm partials (z.x, z.z, x.x): per-CTA chains over a fixed grid
+//     (norm_tiles), one block tree per CTA;
 //   * a column total over tiles is block_totals(): thread k adds the tiles
 //     k, k+256, k+512, ... in ascending order, then the warp xor butterfly
 //     and the 8 warps in ascending order.
@@ -45,10 +46,25 @@ __host__ __device__ inline int64_t num_tiles(int64_t m) {
     const int64_t t = tile_rows(m);
     return (m + t - 1) / t;
 }
-// The norm partials (z.x, z.z, x.x) use 256-row tiles (thread k owns row k,
-// block tree), so the fine-grained SpMV can emit them; their totals are
-// block_totals over ceil(m / 256) partials.
-__host__ __device__ inline int64_t norm_tiles(int64_t m) { return (m + kBlock - 1) / kBlock; }
+// The norm partials (z.x, z.z, x.x) are formed by a FIXED grid of
+// norm_tiles(m) = min(ceil(m/256), kNormGrid) CTAs: CTA b owns the 256-row
+// blocks b, b+G, b+2G, ...; thread k accumulates (fma) its row k of each owned
+// block in ascending block order; one block tree (warp xor butterfly, warps
+// ascending) per CTA gives partial b.  No barrier inside the row loop, one
+// per CTA at the end.  Totals are block_totals over the G partials.
+constexpr int kNormGrid = 148 * 8;
+__host__ __device__ inline int64_t norm_tiles(int64_t m) {
+    const int64_t b = (m + kBlock - 1) / kBlock;
+    return b < kNormGrid ? b : kNormGrid;
+}
+
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start (launch, prologue) while
+// its predecessor drains; pdl_wait() blocks until the predecessor grid has
+// completed and its memory is visible, pdl_trigger() lets the successor
+// launch.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ bool failed(const int32_t *status) {
     return status != nullptr && *(volatile const int32_t *)status >= 0;
@@ -168,37 +184,26 @@ struct NormOut {
     int32_t *status;
 };
 
-// Norm partials of 256-row tiles.  norm_sub_partial(g, ...) is called by
-// every thread for each of NT consecutive tiles tile0 + g (this thread's
-// (z.x, z.z, x.x) terms of row (tile0+g)*256 + k, zero past m);
-// norm_tiles_finish<NT>() then forms the NT partials with the block_sum tree
-// (warp xor butterfly, warps in ascending order), one barrier pair.
-__device__ __forceinline__ void norm_sub_partial(int g, double t, double zz, double xx,
-                                                 double *sm /* [NT*3*kWarps] */) {
+// Norm partial of this CTA (all kBlock threads call it once, with their
+// accumulated chains): block tree, then partial blockIdx.x of each term.
+__device__ __forceinline__ void norm_cta_partial(const NormOut &o, double t, double zz, double xx) {
+    __shared__ double sm[3 * kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     t = warp_sum(t);
     zz = warp_sum(zz);
     xx = warp_sum(xx);
     if (lane == 0) {
-        sm[(g * 3 + 0) * kWarps + warp] = t;
-        sm[(g * 3 + 1) * kWarps + warp] = zz;
-        sm[(g * 3 + 2) * kWarps + warp] = xx;
+        sm[0 * kWarps + warp] = t;
+        sm[1 * kWarps + warp] = zz;
+        sm[2 * kWarps + warp] = xx;
     }
-}
-
-template <int NT>
-__device__ __forceinline__ void norm_tiles_finish(const NormOut &o, int64_t tile0, double *sm) {
     __syncthreads();
-    if (threadIdx.x < 3 * NT) {
-        const int g = threadIdx.x / 3, k = threadIdx.x % 3;
-        if (tile0 + g < o.ntiles) {
-            double s = sm[(g * 3 + k) * kWarps];
+    if (threadIdx.x < 3) {
+        double s = sm[threadIdx.x * kWarps];
 #pragma unroll
-            for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, sm[(g * 3 + k) * kWarps + w]);
-            o.npart[(int64_t)k * o.ntiles + tile0 + g] = s;
-        }
+        for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, sm[threadIdx.x * kWarps + w]);
+        o.npart[(int64_t)threadIdx.x * o.ntiles + blockIdx.x] = s;
     }
-    __syncthreads();
 }
 
 // After a CTA wrote all its tiles' partials: the last CTA of the grid forms
@@ -234,23 +239,25 @@ struct ColArgs {
     NormOut out;          // out.npart == nullptr: update only
 };
 
-// Grid-stride over groups of kColTiles consecutive 256-row norm tiles
-// (thread k owns row k of each; all loads of a group in flight together),
-// one barrier pair per group, one completion ticket per CTA.
+// Column update (+ norm chains when out.npart): launched with exactly
+// norm_tiles(m) CTAs (the canonical norm grid); kColTiles owned blocks are
+// processed per iteration with all their loads in flight, rows accumulated
+// in ascending block order.
 constexpr int kColTiles = 4;
-__global__ void __launch_bounds__(kBlock) col_update_norm_kernel(ColArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
+    pdl_wait();
     if (failed(a.out.status)) return;
-    __shared__ double sm[kColTiles * 3 * kWarps];
     const bool upd = a.r != nullptr;
     const double rj = upd ? *a.r : 0.0;
-    const int64_t ntiles = (a.m + kBlock - 1) / kBlock;
-    for (int64_t tile0 = (int64_t)blockIdx.x * kColTiles; tile0 < ntiles;
-         tile0 += (int64_t)gridDim.x * kColTiles) {
+    const int64_t nblk = (a.m + kBlock - 1) / kBlock;
+    const int64_t G = gridDim.x;
+    double t = 0.0, zz = 0.0, xx = 0.0;
+    for (int64_t b0 = blockIdx.x; b0 < nblk; b0 += G * kColTiles) {
         double z[kColTiles], xv[kColTiles], q[kColTiles], pp[kColTiles];
 #pragma unroll
         for (int g = 0; g < kColTiles; ++g) {  // loads first
-            const int64_t r = (tile0 + g) * kBlock + threadIdx.x;
-            const bool ok = r < a.m;
+            const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
+            const bool ok = b0 + g * G < nblk && r < a.m;
             z[g] = ok ? a.z[r] : 0.0;
             q[g] = (ok && upd) ? a.qprev[r] : 0.0;
             xv[g] = ok ? (a.x ? a.x[r] : (a.xnorm ? a.xnorm[r] : 0.0)) : 0.0;
@@ -258,8 +265,8 @@ __global__ void __launch_bounds__(kBlock) col_update_norm_kernel(ColArgs a) {
         }
 #pragma unroll
         for (int g = 0; g < kColTiles; ++g) {
-            const int64_t r = (tile0 + g) * kBlock + threadIdx.x;
-            const bool ok = r < a.m;
+            const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
+            const bool ok = b0 + g * G < nblk && r < a.m;
             if (upd) {
                 z[g] = __dsub_rn(z[g], __dmul_rn(rj, q[g]));
                 if (ok) a.z[r] = z[g];
@@ -268,13 +275,17 @@ __global__ void __launch_bounds__(kBlock) col_update_norm_kernel(ColArgs a) {
                     if (ok) a.x[r] = xv[g];
                 }
             }
-            if (a.out.npart != nullptr)
-                norm_sub_partial(g, ok ? fma(z[g], xv[g], 0.0) : 0.0, ok ? fma(z[g], z[g], 0.0) : 0.0,
-                                 ok ? fma(xv[g], xv[g], 0.0) : 0.0, sm);
+            if (ok) {
+                t = fma(z[g], xv[g], t);
+                zz = fma(z[g], z[g], zz);
+                xx = fma(xv[g], xv[g], xx);
+            }
         }
-        if (a.out.npart != nullptr) norm_tiles_finish<kColTiles>(a.out, tile0, sm);
     }
-    if (a.out.npart != nullptr) norm_last_cta(a.out);
+    pdl_trigger();
+    if (a.out.npart == nullptr) return;  // uniform
+    norm_cta_partial(a.out, t, zz, xx);
+    norm_last_cta(a.out);
 }
 
 // Standalone totals of the norm partials (step API / multi-GPU driver).
@@ -376,24 +387,33 @@ template <int RPT, bool HP>
 __device__ __forceinline__ void trail_vectors(const TrailArgs &a, int64_t row0, bool store,
                                               double *q, double *p, double *pp) {
     const bool upd = a.qprev != nullptr;
+    const bool sq = store && a.qout != nullptr, sp = store && a.pout != nullptr;
+    // all loads first (the stores below may alias them as far as the
+    // compiler knows: interleaving would serialize RPT round trips)
+    double ps[RPT], zs[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t r = row0 + (int64_t)u * kBlock;
+        const bool ok = r < a.m;
+        ps[u] = ok ? a.psrc[r] : 0.0;
+        q[u] = (ok && upd) ? a.qprev[r] : 0.0;
+        pp[u] = (HP && ok && upd) ? a.pprev[r] : 0.0;
+        zs[u] = (ok && sq) ? a.zsrc[r] : 0.0;
+    }
     const double rii = a.rii ? *a.rii : 1.0;
 #pragma unroll
     for (int u = 0; u < RPT; ++u) {
         const int64_t r = row0 + (int64_t)u * kBlock;
         const bool ok = r < a.m;
-        const double ps = ok ? a.psrc[r] : 0.0;
-        p[u] = a.rii ? ps / rii : ps;
-        q[u] = (ok && upd) ? a.qprev[r] : 0.0;
-        pp[u] = (HP && ok && upd) ? a.pprev[r] : 0.0;
-        if (store && ok) {
-            if (a.qout) a.qout[r] = a.zsrc[r] / rii;
-            if (a.pout) a.pout[r] = p[u];
-        }
+        p[u] = a.rii ? ps[u] / rii : ps[u];
+        if (ok && sq) a.qout[r] = zs[u] / rii;
+        if (ok && sp) a.pout[r] = p[u];
     }
 }
 
 template <int RPT, int CU, bool HP, bool CGS>
 __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
+    pdl_wait();
     if (failed(a.status)) return;
     extern __shared__ double wsum[];  // [kWarps][cpg]
     const int tile = blockIdx.x;
@@ -452,6 +472,7 @@ __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
             if (lane == 0 && j0 + c < cend) wsum[warp * a.cpg + (j0 + c - cbeg)] = s;
         }
     }
+    pdl_trigger();
     __syncthreads();
     for (int c = threadIdx.x; c < cend - cbeg; c += kBlock) {
         double s = wsum[c];
@@ -581,7 +602,7 @@ struct RunWalker {
 template <bool HP, bool CGS, bool HINT>
 __global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs a) {
     using C = TmaCfg<HP, CGS>;
-    if (failed(a.status)) return;
+
     extern __shared__ __align__(128) unsigned char smem[];
     double *stage_buf = reinterpret_cast<double *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)C::kStages * C::kStageBytes);
@@ -603,6 +624,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs 
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    pdl_wait();  // everything below reads the predecessors' results
+    if (failed(a.status)) return;
     for (int c = threadIdx.x; c < t; c += kTmaThreads) rsm[c] = upd ? a.rprev[a.jbeg + c] : 0.0;
     __syncthreads();
 
@@ -706,6 +729,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs 
             }
             consumer_bar();
         }
+        pdl_trigger();
         // ---- r row totals: the last min(t, grid) CTAs to finish reduce ----
         if (a.counters != nullptr && t > 0) {
             const unsigned G = gridDim.x;
@@ -827,23 +851,23 @@ __device__ __forceinline__ double csr_row(const CsrArgs &a, const double *x, int
 // R rows at once: when every row has <= kRowBatch nonzeros, all R rows'
 // (index, value) loads are issued together, then all R x R gathers, then the
 // sums in stored order; otherwise row by row (csr_row).  Same arithmetic.
-template <int R>
+template <int R, int B = kRowBatch>
 __device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], const int (&e)[R],
                                          bool upd, double rj, double (&y)[R]) {
     bool short_rows = true;
 #pragma unroll
-    for (int i = 0; i < R; ++i) short_rows &= (e[i] - s[i] <= kRowBatch);
+    for (int i = 0; i < R; ++i) short_rows &= (e[i] - s[i] <= B);
     if (!short_rows) {
 #pragma unroll
         for (int i = 0; i < R; ++i) y[i] = csr_row(a, a.X, s[i], e[i], upd, rj);
         return;
     }
-    int c[R][kRowBatch];
-    double v[R][kRowBatch], xv[R][kRowBatch];
+    int c[R][B];
+    double v[R][B], xv[R][B];
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int h = 0; h < kRowBatch; ++h) {
+        for (int h = 0; h < B; ++h) {
             const bool ok = s[i] + h < e[i];
             c[i][h] = ok ? __ldg(a.indices + s[i] + h) : 0;
             v[i][h] = ok ? __ldg(a.data + s[i] + h) : 0.0;
@@ -851,7 +875,7 @@ __device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], co
 #pragma unroll
     for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int h = 0; h < kRowBatch; ++h) {
+        for (int h = 0; h < B; ++h) {
             const bool ok = s[i] + h < e[i];
             xv[i][h] = ok ? __ldg(a.X + c[i][h]) : 0.0;
             if (upd && ok) xv[i][h] = __dsub_rn(xv[i][h], __dmul_rn(rj, __ldg(a.qprev + c[i][h])));
@@ -860,7 +884,7 @@ __device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], co
     for (int i = 0; i < R; ++i) {
         double acc = 0.0;
 #pragma unroll
-        for (int h = 0; h < kRowBatch; ++h)
+        for (int h = 0; h < B; ++h)
             if (s[i] + h < e[i]) acc = __dadd_rn(acc, __dmul_rn(v[i][h], xv[i][h]));
         y[i] = acc;
     }
@@ -901,33 +925,44 @@ __global__ void __launch_bounds__(kBlock) csr_row_kernel(CsrArgs a) {
     }
 }
 
-// Fused HA/naive step: grid-stride over the 256-row norm tiles, one row per
-// thread, one barrier pair per tile, one completion ticket per CTA.
-__global__ void __launch_bounds__(kBlock) csr_step_kernel(CsrArgs a) {
+// Fused HA/naive step, launched with exactly norm_tiles(m) CTAs (the
+// canonical norm grid): CTA b handles rows of the 256-row blocks b, b+G, ...
+// one per thread, accumulating the norm chains in ascending block order; the
+// next row's pointers are prefetched; one block tree per CTA at the end.
+template <int B, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
+    pdl_wait();
     if (failed(a.out.status)) return;
-    __shared__ double sm[3 * kWarps];
     const bool upd = a.r != nullptr;
     const double rj = upd ? *a.r : 0.0;
-    const int64_t ntiles = (a.m + kBlock - 1) / kBlock;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t row = tile * kBlock + threadIdx.x;
-        const bool ok = row < a.m;
-        int s[1], e[1];
-        double y[1];
-        s[0] = ok ? __ldg(a.indptr + row) : 0;
-        e[0] = ok ? __ldg(a.indptr + row + 1) : 0;
-        csr_rows<1>(a, s, e, upd, rj, y);
-        double z = 0.0;
-        if (ok) {
-            z = a.X[row];
+    const int64_t nblk = (a.m + kBlock - 1) / kBlock;
+    const int64_t G = gridDim.x;
+    double t = 0.0, zz = 0.0, xx = 0.0;
+    int64_t row = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    int s = row < a.m ? __ldg(a.indptr + row) : 0;
+    int e = row < a.m ? __ldg(a.indptr + row + 1) : 0;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += G) {
+        const int64_t nrow = row + G * kBlock;  // prefetch the next owned row's pointers
+        const int ns = nrow < a.m ? __ldg(a.indptr + nrow) : 0;
+        const int ne = nrow < a.m ? __ldg(a.indptr + nrow + 1) : 0;
+        if (row < a.m) {
+            int sa[1] = {s}, ea[1] = {e};
+            double y[1];
+            csr_rows<1, B>(a, sa, ea, upd, rj, y);
+            double z = a.X[row];
             if (upd) z = __dsub_rn(z, __dmul_rn(rj, a.qprev[row]));
             a.Y[row] = y[0];
             if (a.znew) a.znew[row] = z;
+            t = fma(z, y[0], t);
+            zz = fma(z, z, zz);
+            xx = fma(y[0], y[0], xx);
         }
-        norm_sub_partial(0, ok ? fma(z, y[0], 0.0) : 0.0, ok ? fma(z, z, 0.0) : 0.0,
-                         ok ? fma(y[0], y[0], 0.0) : 0.0, sm);
-        norm_tiles_finish<1>(a.out, tile, sm);
+        row = nrow;
+        s = ns;
+        e = ne;
     }
+    pdl_trigger();
+    norm_cta_partial(a.out, t, zz, xx);
     norm_last_cta(a.out);
 }
 

@@ -216,9 +216,7 @@ class CsrSpdOperator(SpdOperator):
             raise DimensionError("column index out of range")
         super().__init__(m)
         self._check_int32(m, nnz)
-        dev = D.device()
-        self._dev = (indptr.to(dev, t.int32).contiguous(), indices.to(dev, t.int32).contiguous(),
-                     data.to(dev, t.float64).contiguous())
+        self._dev = _pack_csr(indptr, indices, data)
         self.indptr, self.indices, self.data = indptr, indices, data
 
     @staticmethod
@@ -233,16 +231,12 @@ class CsrSpdOperator(SpdOperator):
     def _device_arrays(self):
         if self._dev is None:
             self._check_int32(self.dim, self.nnz)
-            t = D.torch()
-            dev = D.device()
-            self._dev = (t.from_numpy(self.indptr.astype(np.int32)).to(dev),
-                         t.from_numpy(self.indices.astype(np.int32)).to(dev),
-                         t.from_numpy(self.data).to(dev))
+            self._dev = _pack_csr(self.indptr, self.indices, self.data)
         return self._dev
 
     def _native(self):
         if self._desc is None:
-            ip, ix, dv = self._device_arrays()
+            ip, ix, dv, _ = self._device_arrays()
             d = _lib.AqrOp()
             d.kind = _lib.AQR_OP_CSR
             d.spmv_lanes = self.spmv_lanes
@@ -260,6 +254,29 @@ class CsrSpdOperator(SpdOperator):
         rows = np.repeat(np.arange(self.dim), np.diff(indptr))
         np.add.at(A, (rows, indices), data)
         return A
+
+
+def _pack_csr(indptr, indices, data):
+    """Device copies (int32 indptr, int32 indices, fp64 data) in ONE allocation.
+
+    values first, then indices, then row pointers: one contiguous range the
+    factorization can mark L2-persisting (aqr_gs_factor, l2_window_begin).
+    """
+    t = D.torch()
+    dev = D.device()
+    nnz, m1 = int(data.shape[0]), int(indptr.shape[0])
+    off_i = 8 * nnz
+    off_p = off_i + 4 * nnz + (4 * nnz) % 8
+    buf = t.empty(off_p + 4 * m1 + 16, dtype=t.uint8, device=dev)
+    dv = buf[:off_i].view(t.float64)
+    ix = buf[off_i:off_i + 4 * nnz].view(t.int32)
+    ip = buf[off_p:off_p + 4 * m1].view(t.int32)
+    as_t = (lambda a, dt: a.to(dev, dt)) if D.is_torch(data) else \
+        (lambda a, dt: t.from_numpy(np.ascontiguousarray(a)).to(dev, dt))
+    dv.copy_(as_t(data, t.float64))
+    ix.copy_(as_t(indices, t.int32))
+    ip.copy_(as_t(indptr, t.int32))
+    return ip, ix, dv, buf
 
 
 def csr_from_coo(dim, rows, cols, values):

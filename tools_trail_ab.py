@@ -31,3 +31,13 @@ for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update")):
                      "GBps": b.value / (ms.value / 1e3) / 1e9}
 L.aqr_trailing_timer_enable(0)
 print(json.dumps(out))
+if os.environ.get("AQR_LIST"):
+    import numpy as np
+    L.aqr_trailing_timer_enable(1)
+    aqr.factorize(Zd, op, meth)
+    torch.cuda.synchronize()
+    ms = np.zeros(512); by = np.zeros(512)
+    k = L.aqr_kernel_timer_list(0, ms.ctypes.data, by.ctypes.data, 512)
+    for j in range(k):
+        print(f"launch {j:3d} us {1e3*ms[j]:8.1f} MB {by[j]/1e6:8.1f} GB/s {by[j]/(ms[j]/1e3)/1e9:7.0f} ideal_us {by[j]/6554.9e9*1e6:7.1f}")
+    L.aqr_trailing_timer_enable(0)
