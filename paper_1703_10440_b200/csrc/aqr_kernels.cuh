@@ -76,6 +76,59 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Warp totals of 8 values per lane (8 columns) at once, by a transposed
+// butterfly: round 1 (xor 16) keeps 4 columns per lane, round 2 (xor 8) 2,
+// round 3 (xor 4) 1, rounds 4-5 (xor 2, 1) finish.  Every column is summed
+// over the same hypercube tree as warp_sum (16, 8, 4, 2, 1 -- IEEE addition
+// is commutative), so the totals are bitwise warp_sum's, with 9 shuffles
+// instead of 40.  Lane l returns the total of column (l >> 2).
+__device__ __forceinline__ double warp_sum8(const double (&v)[8]) {
+    const int lane = threadIdx.x & 31;
+    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+    double a4[4], a2[2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double keep = b4 ? v[4 + k] : v[k], send = b4 ? v[k] : v[4 + k];
+        a4[k] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double keep = b3 ? a4[2 + k] : a4[k], send = b3 ? a4[k] : a4[2 + k];
+        a2[k] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+    }
+    const double keep = b2 ? a2[1] : a2[0], send = b2 ? a2[0] : a2[1];
+    double c = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+    c = __dadd_rn(c, __shfl_xor_sync(0xffffffffu, c, 2));
+    c = __dadd_rn(c, __shfl_xor_sync(0xffffffffu, c, 1));
+    return c;
+}
+
+// Same for 4 columns (xor 16 keeps 2, xor 8 keeps 1, then 4, 2, 1); lane l
+// returns the total of column (l >> 3).
+__device__ __forceinline__ double warp_sum4(const double (&v)[4]) {
+    const int lane = threadIdx.x & 31;
+    const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+    double a2[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double keep = b4 ? v[2 + k] : v[k], send = b4 ? v[k] : v[2 + k];
+        a2[k] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+    const double keep = b3 ? a2[1] : a2[0], send = b3 ? a2[0] : a2[1];
+    double c = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+    c = __dadd_rn(c, __shfl_xor_sync(0xffffffffu, c, 4));
+    c = __dadd_rn(c, __shfl_xor_sync(0xffffffffu, c, 2));
+    c = __dadd_rn(c, __shfl_xor_sync(0xffffffffu, c, 1));
+    return c;
+}
+
+template <int NB>
+__device__ __forceinline__ double warp_sum_batch(const double (&v)[NB]);
+template <>
+__device__ __forceinline__ double warp_sum_batch<8>(const double (&v)[8]) { return warp_sum8(v); }
+template <>
+__device__ __forceinline__ double warp_sum_batch<4>(const double (&v)[4]) { return warp_sum4(v); }
+
 // Fixed-order block sum over kBlock threads; every thread returns the value.
 __device__ __forceinline__ double block_sum(double v, double *smem /* kWarps */) {
     v = warp_sum(v);
@@ -673,7 +726,16 @@ __global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs 
             }
             if (t == 0) continue;
             const bool tma = tile < full_tiles;
-            for (int cc = 0; cc < c1 - c0; ++cc) {
+            const int ncols = c1 - c0;
+            // columns in batches of NB: one batched warp reduction per batch
+            constexpr int NB = (HP || CGS) ? 4 : 8;
+            for (int cc0 = 0; cc0 < ncols; cc0 += NB) {
+              double bacc[NB];
+#pragma unroll
+              for (int k = 0; k < NB; ++k) {
+                bacc[k] = 0.0;
+                const int cc = cc0 + k;
+                if (cc >= ncols) continue;
                 const int jr = a.reverse ? c1 - 1 - cc : c0 + cc;  // column relative to jbeg
                 const int j = a.jbeg + jr;
                 const double rj = rsm[jr];
@@ -717,8 +779,13 @@ __global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs 
                     }
                     acc = fma(p[u], CGS ? d[u] : z[u], acc);
                 }
-                acc = warp_sum(acc);
-                if (lane == 0) wsum[warp * kTmaMaxCols + jr] = acc;
+                bacc[k] = acc;
+              }
+              // batched warp reduction of the NB columns (same tree as warp_sum)
+              const double tot = warp_sum_batch<NB>(bacc);
+              const int cc = cc0 + lane / (32 / NB);
+              if (lane % (32 / NB) == 0 && cc < ncols)
+                  wsum[warp * kTmaMaxCols + (a.reverse ? c1 - 1 - cc : c0 + cc)] = tot;
             }
             consumer_bar();
             for (int c = c0 + threadIdx.x; c < c1; c += kBlock) {
