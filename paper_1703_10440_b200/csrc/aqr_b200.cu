@@ -260,6 +260,14 @@ aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx
     const int64_t m = op->m;
     const int64_t ncols = op->ncols > 0 ? op->ncols : m;
     if (m == 0) return AQR_OK;
+    const bool tma_ok = m % 2 == 0 && ncols % 2 == 0 && op->lda % 2 == 0 &&
+                        (uintptr_t)op->A % 16 == 0 && (uintptr_t)X % 16 == 0;
+    if (k == 1 && tma_ok) {
+        AQR_TRY(ensure_smem(aqr::dense_gemv_tma_kernel, aqr::kGvSmem));
+        aqr::dense_gemv_tma_kernel<<<(unsigned)((m + aqr::kGvRows - 1) / aqr::kGvRows), aqr::kGvRows + 32,
+                                     aqr::kGvSmem, s>>>(m, ncols, op->A, op->lda, X, Y);
+        return launched("dense_gemv_tma_kernel");
+    }
     if (k == 1) {
         dim3 grid((unsigned)((m + aqr::kGemvBlock - 1) / aqr::kGemvBlock), 1);
         aqr::dense_gemv_kernel<<<grid, aqr::kGemvBlock, 0, s>>>(m, ncols, op->A, op->lda, X, ldx, Y, ldy);

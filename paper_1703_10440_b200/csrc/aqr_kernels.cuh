@@ -1039,34 +1039,120 @@ __global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
 // y = A x, one thread per row, ascending j, separately rounded (bitwise equal
 // to matvec, _kernels_impl.py:24-32).  Loads of A are coalesced across the
 // warp (column-major); x is staged in shared memory in chunks.
-constexpr int kGemvBlock = 128;
-constexpr int kGemvChunk = 2048;
+constexpr int kGemvBlock = 64;
+constexpr int kGemvU = 16;
+// Software-pipelined: the next 16 columns of A are in flight while the
+// current 16 are accumulated (32 loads per thread outstanding); x[j] is a
+// warp-uniform (broadcast) load.  With one row per thread, m = 32768 gives
+// only ~7 warps per SM, so the loads in flight per thread set the bandwidth.
 __global__ void __launch_bounds__(kGemvBlock)
     dense_gemv_kernel(int64_t m, int64_t ncols, const double *__restrict__ A, int64_t lda,
                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y,
                       int64_t ldy) {
-    __shared__ double xs[kGemvChunk];
+    constexpr int U = kGemvU;
     const int64_t row = blockIdx.x * (int64_t)kGemvBlock + threadIdx.x;
+    if (row >= m) return;
     const double *x = X + blockIdx.y * ldx;
-    const double *arow = A + min(row, m - 1);
+    const double *arow = A + row;
     double acc = 0.0;
-    constexpr int U = 16;
-    for (int64_t j0 = 0; j0 < ncols; j0 += kGemvChunk) {
-        const int len = (ncols - j0) < kGemvChunk ? (int)(ncols - j0) : kGemvChunk;
-        __syncthreads();
-        for (int q = threadIdx.x; q < len; q += kGemvBlock) xs[q] = __ldg(x + j0 + q);
-        __syncthreads();
-        int j = 0;
-        for (; j + U <= len; j += U) {
-            double av[U];
+    const int64_t full = ncols / U * U;
+    double a0[U], a1[U];
+    if (full > 0) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) av[u] = __ldg(arow + (j0 + j + u) * lda);
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(av[u], xs[j + u]));
-        }
-        for (; j < len; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(arow + (j0 + j) * lda), xs[j]));
+        for (int u = 0; u < U; ++u) a0[u] = __ldg(arow + u * lda);
     }
-    if (row < m) Y[row + blockIdx.y * ldy] = acc;
+    for (int64_t j = 0; j < full; j += 2 * U) {
+        const bool has1 = j + U < full, has2 = j + 2 * U < full;
+        if (has1) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) a1[u] = __ldg(arow + (j + U + u) * lda);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(a0[u], __ldg(x + j + u)));
+        if (!has1) break;
+        if (has2) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) a0[u] = __ldg(arow + (j + 2 * U + u) * lda);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(a1[u], __ldg(x + j + U + u)));
+    }
+    for (int64_t j = full; j < ncols; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(arow + j * lda), __ldg(x + j)));
+    Y[row + blockIdx.y * ldy] = acc;
+}
+
+// y = A x streamed by TMA (the north star's "x staged in shared memory"):
+// a CTA owns kGvRows rows; one producer warp streams kGvCols-column panels
+// of A (kGvCols bulk copies of one column segment each, contiguous in the
+// column-major layout) plus the matching slice of x into a kGvStages-deep
+// shared-memory ring with mbarrier transaction counts; consumer thread r
+// accumulates row r over ascending j from shared memory -- the reference's
+// order, bitwise matvec.  The bytes in flight no longer depend on registers
+// (one row per thread gives only ~7 warps per SM at m = 32768).
+// Requires lda, m even (16-byte-aligned segments); else dense_gemv_kernel.
+constexpr int kGvRows = 128, kGvCols = 32, kGvStages = 3;
+constexpr size_t kGvStageBytes = (size_t)kGvRows * kGvCols * 8 + kGvCols * 8;
+constexpr size_t kGvSmem = kGvStages * kGvStageBytes + 2 * kGvStages * 8;
+__device__ __forceinline__ void gv_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kGvRows + 32, 2)
+    dense_gemv_tma_kernel(int64_t m, int64_t ncols, const double *__restrict__ A, int64_t lda,
+                          const double *__restrict__ x, double *__restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kGvStages * kGvStageBytes);
+    uint64_t *empty = full + kGvStages;
+    const int64_t r0 = (int64_t)blockIdx.x * kGvRows;
+    const int rows = (m - r0) < kGvRows ? (int)(m - r0) : kGvRows;
+    const int64_t ntile = (ncols + kGvCols - 1) / kGvCols;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kGvStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kGvRows / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kGvRows / 32) {  // producer
+        if (lane == 0) {
+            for (int64_t t = 0; t < ntile; ++t) {
+                const int s = (int)(t % kGvStages);
+                const uint32_t ph = (uint32_t)((t / kGvStages) & 1);
+                const int64_t j0 = t * kGvCols;
+                const int cols = (ncols - j0) < kGvCols ? (int)(ncols - j0) : kGvCols;
+                mbar_wait(empty + s, ph ^ 1);
+                mbar_expect_tx(full + s, (uint32_t)(cols * rows * 8 + ((cols * 8 + 15) & ~15)));
+                double *dst = reinterpret_cast<double *>(smem + s * kGvStageBytes);
+                for (int c = 0; c < cols; ++c)
+                    bulk_g2s<false>(dst + c * kGvRows, A + r0 + (j0 + c) * lda, (uint32_t)(rows * 8),
+                                    full + s, 0);
+                bulk_g2s<false>(dst + kGvRows * kGvCols, x + j0, (uint32_t)((cols * 8 + 15) & ~15),
+                                full + s, 0);
+            }
+        }
+        return;
+    }
+    double acc = 0.0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        const int s = (int)(t % kGvStages);
+        const uint32_t ph = (uint32_t)((t / kGvStages) & 1);
+        const int64_t j0 = t * kGvCols;
+        const int cols = (ncols - j0) < kGvCols ? (int)(ncols - j0) : kGvCols;
+        mbar_wait(full + s, ph);
+        const double *src = reinterpret_cast<const double *>(smem + s * kGvStageBytes);
+        const double *xs = src + kGvRows * kGvCols;
+        if (cols == kGvCols) {
+#pragma unroll
+            for (int c = 0; c < kGvCols; ++c)
+                acc = __dadd_rn(acc, __dmul_rn(src[c * kGvRows + threadIdx.x], xs[c]));
+        } else {
+            for (int c = 0; c < cols; ++c)
+                acc = __dadd_rn(acc, __dmul_rn(src[c * kGvRows + threadIdx.x], xs[c]));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+    if (threadIdx.x < rows) y[r0 + threadIdx.x] = acc;
 }
 
 // Y = A X (k columns), shared-memory tiled, every output accumulated over
