@@ -242,16 +242,24 @@ def run_b200(args, rank, world, local_rank):
     peak, peak_kind = measured_peaks()
     achieved = (kbytes.value / nl.value) / (kms.value / nl.value / 1e3) / 1e9 if nl.value else None
     share = (kms.value / args.steps) / ms_per_step if nl.value else None
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "trailing_traffic.json")
-    if os.path.exists(tpath):
+    # DRAM traffic of the same kernel from the committed ncu --set full capture
+    # (profiles/<round>/trailing_traffic.json, tools/ncu_summary.py): measured
+    # DRAM bytes / algorithmic bytes of the captured launches, applied to
+    # this run's mean algorithmic bytes per launch.
+    traffic, traffic_src = None, None
+    import glob
+
+    for tpath in sorted(glob.glob(os.path.join(REPO, "profiles", "r*", "trailing_traffic.json")))[::-1]:
         with open(tpath) as f:
             tt = json.load(f)
-        if tt.get("method") == args.method:
-            traffic = tt.get("dram_bytes_per_launch")
+        if tt.get("method") == args.method and tt.get("traffic_over_algorithmic") and nl.value:
+            traffic = tt["traffic_over_algorithmic"] * kbytes.value / nl.value / 1e9
+            traffic_src = os.path.relpath(tpath, REPO)
+            break
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak if achieved else None, "traffic": traffic,
+        "traffic_unit": "GB per launch (DRAM read+write)", "traffic_source": traffic_src,
         "kernel": "trailing_kernel", "peak_source": f"{peak_kind} hbm_gbs",
         "launches_per_step": nl.value / args.steps if nl.value else 0,
         "kernel_ms_per_step": kms.value / args.steps, "kernel_share_of_step": share,

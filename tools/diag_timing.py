@@ -1,7 +1,7 @@
 """Diagnostics: host enqueue time vs device time of one factorization (AQR_DEBUG_TIMING)."""
 import os, sys, time
 os.environ["AQR_DEBUG_TIMING"] = "1"
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1703_10440_b200 as aqr
 from paper_1703_10440_b200 import problems

@@ -1,6 +1,6 @@
 """Diagnostics: host<->device transfer costs of the e2e path (config 2 sizes)."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1703_10440_b200 as aqr
 from paper_1703_10440_b200 import problems

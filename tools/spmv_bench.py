@@ -1,6 +1,6 @@
 """Diagnostics: plain SpMV / SpMM timing on config 2 (device-resident)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1703_10440_b200 as aqr
 from paper_1703_10440_b200 import problems
