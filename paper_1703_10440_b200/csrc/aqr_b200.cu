@@ -211,8 +211,10 @@ aqr::NormOut no_norm() {
 
 aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                       int64_t ldy, const double *qprev, const double *r, double *znew,
-                      const aqr::NormOut &out, cudaStream_t s) {
+                      const aqr::NormOut &out, cudaStream_t s, const aqr::RrowIn *rin = nullptr) {
     aqr::CsrArgs a;
+    std::memset(&a.rin, 0, sizeof a.rin);
+    if (rin && out.npart != nullptr) a.rin = *rin;
     a.m = op->m;
     a.k = k;
     a.indptr = op->indptr;
@@ -312,8 +314,11 @@ aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, d
 
 aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
                                   const double *pprev, const double *r, const double *xnorm,
-                                  const aqr::NormOut &out, cudaStream_t s) {
+                                  const aqr::NormOut &out, cudaStream_t s,
+                                  const aqr::RrowIn *rin = nullptr) {
     aqr::ColArgs a;
+    std::memset(&a.rin, 0, sizeof a.rin);
+    if (rin) a.rin = *rin;
     a.m = m;
     a.z = z;
     a.qprev = qprev;
@@ -361,7 +366,11 @@ int choose_cpg_generic(int64_t ntiles, int64_t ncols) {
 aqr_status launch_rrow_reduce(int64_t m, int64_t ncols, const double *partial, double *out,
                               const int32_t *status, cudaStream_t s);
 
-aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStream_t s) {
+// deferred != nullptr: the caller's next norm kernel forms the r-row totals
+// (RrowIn); *deferred tells whether the generic kernel left them pending.
+aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStream_t s,
+                           bool *deferred = nullptr) {
+    if (deferred) *deferred = false;
     aqr::TrailArgs a = a0;
     const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
     if (a.ntiles == 0) return AQR_OK;
@@ -369,7 +378,13 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     const bool aligned = (a.ldw % 2 == 0) && (!hp || a.ldx % 2 == 0) && (!cgs || a.ldz0 % 2 == 0) &&
                          ((uintptr_t)a.W % 16 == 0) && (!hp || (uintptr_t)a.X % 16 == 0) &&
                          (!cgs || (uintptr_t)a.Z0 % 16 == 0);
-    const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && trail_variant() != 2;
+    // Measured on B200 (tools/kernel_ab.py, config 2): the short-lived LDG
+    // kernel plus a separate totals launch beats the persistent TMA-pipelined
+    // kernel for HA (8.84 vs 9.26 ms/factorization) and HP (14.1 vs 14.4 ms).
+    // AQR_TRAIL_VARIANT: 0 = LDG CU=2 (default), 3 = LDG CU=4 (HA),
+    // 1 = TMA without the L2 hint, 4 = TMA with the evict-first hint.
+    const int tv = trail_variant();
+    const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && (tv == 1 || tv == 4);
     a.cpg = tma ? (int32_t)std::max<int64_t>(ncols, 1) : choose_cpg_generic(a.ntiles, ncols);
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
 
@@ -394,7 +409,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
             occ[dev_ & 63] = std::max(1, std::min(o_, 2));                                       \
         }                                                                                        \
         const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sm_count() * occ[dev_ & 63]); \
-        if (trail_variant() == 1)                                                                \
+        if (tv == 1)                                                                             \
             launch_pdl(aqr::trailing_tma_kernel<HP, CGS, false>, grid, aqr::kTmaThreads, smem, s, a); \
         else                                                                                     \
             launch_pdl(aqr::trailing_tma_kernel<HP, CGS, true>, grid, aqr::kTmaThreads, smem, s, a); \
@@ -412,6 +427,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     } while (0)
         if (big) {
             if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
+            else if (tv == 3) { if (cgs) LAUNCH(8, 4, false, true); else LAUNCH(8, 4, false, false); }
             else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
         } else {
             if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
@@ -421,8 +437,13 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     }
     timer_end(tix, s);
     AQR_TRY(launched("trailing_kernel"));
-    if (!tma && a.counters != nullptr)  // generic kernel: totals in a separate launch
+    if (!tma && a.counters != nullptr && ncols > 0) {  // generic kernel: totals pending
+        if (deferred) {
+            *deferred = true;
+            return AQR_OK;
+        }
         return launch_rrow_reduce(a.m, ncols, a.partial, a.rout, a.status, s);
+    }
     return AQR_OK;
 }
 
@@ -473,6 +494,14 @@ aqr_status side_acquire(SideCtx &c) {
 void side_release(const SideCtx &c) {
     std::lock_guard<std::mutex> lk(g_side_mu);
     g_side_free.push_back(c);
+}
+
+int defer_mode() {  // AQR_DEFER=0: separate r-row reduction launch (A/B experiments)
+    static const int v = [] {
+        const char *e = std::getenv("AQR_DEFER");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
 }
 
 int lookahead_mode() {  // AQR_LOOKAHEAD=0 disables (A/B experiments)
@@ -596,8 +625,18 @@ struct Run {
     unsigned *counters;  // [0]: norm, [1 ..]: trailing column groups
     double *Rt, *partial, *npart, *xvec, *zvec, *pvec, *pring, *P, *X, *Z0;
     int64_t mv = 0;
+    bool pending = false;  // row i-1 of R left as trailing partials (RrowIn)
 
     double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
+
+    aqr::RrowIn rrow_in(int64_t j) const {
+        aqr::RrowIn in;
+        in.partial = partial;
+        in.ntiles = (int32_t)aqr::num_tiles(m);
+        in.ncols = (int32_t)(n - j);
+        in.rrow = rt(j - 1, j);
+        return in;
+    }
     double *rt(int64_t i, int64_t j) const { return Rt + i * n + j; }
 
     aqr_status mv1(const double *x, double *y) {
@@ -627,14 +666,18 @@ struct Run {
         double *z = col(W, ldw, j);
         const double *qprev = j > 0 ? col(W, ldw, j - 1) : nullptr;
         const double *r = j > 0 ? rt(j - 1, j) : nullptr;
+        const aqr::RrowIn rin = rrow_in(j);
+        const aqr::RrowIn *pin = pending ? &rin : nullptr;
+        pending = false;
         if (hp) {
             double *x = col(X, m, j);
-            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), s));
+            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), s, pin));
             zcol = z;
             xcol = x;
         } else if (csr_native) {
-            // one fused launch: gather (z - r q), x = A z, z_new, norm, r_jj
-            AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s));
+            // one fused launch: r_{j-1,j} (and the rest of row j-1 of R),
+            // gather (z - r q), x = A z, z_new, norm, r_jj
+            AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s, pin));
             ++mv;
             zcol = zvec;
             xcol = xvec;
@@ -695,7 +738,8 @@ struct Run {
             {
                 static const bool dbg = std::getenv("AQR_DEBUG_TIMING") != nullptr;
                 const auto h0 = std::chrono::steady_clock::now();
-                AQR_TRY(launch_trailing(t, hp, cgs, s));
+                const bool can_defer = (hp || csr_native) && i + 1 < n && defer_mode() != 0;
+                AQR_TRY(launch_trailing(t, hp, cgs, s, can_defer ? &pending : nullptr));
                 if (dbg) {
                     const auto h1 = std::chrono::steady_clock::now();
                     std::fprintf(stderr, "  step %ld trailing launch host %.1f us, norm-step host %.1f us\n", (long)i,

@@ -278,6 +278,34 @@ __device__ __forceinline__ void norm_last_cta(const NormOut &o) {
     }
 }
 
+// Deferred r-row totals.  The trailing pass of step i-1 leaves per-tile
+// partials of r_{i-1,j}, j = i .. n-1; instead of a separate reduction
+// launch, the next norm kernel (step i) forms them: every CTA reduces column
+// i (r_{i-1,i} is needed by all of its rows) and CTA b >= 1 also reduces
+// column i+b.  Same block_totals tree as rrow_reduce_kernel: bitwise equal.
+struct RrowIn {
+    const double *partial;  // [ncols][ntiles]; nullptr: r_{i-1,i} is read from *r
+    int32_t ntiles, ncols;
+    double *rrow;  // rrow[b] = Rt[i-1][i+b]
+};
+
+__device__ __forceinline__ double rrow_first(const RrowIn &in) {
+    __shared__ double tot1[1];
+    __shared__ double sm1[kWarps];
+    block_totals<1>(in.partial, in.ntiles, in.ntiles, tot1, sm1, SyncAll());
+    const double r = tot1[0];
+    if (blockIdx.x == 0 && threadIdx.x == 0) in.rrow[0] = r;
+    return r;
+}
+
+__device__ __forceinline__ void rrow_rest(const RrowIn &in) {
+    if (in.partial == nullptr) return;
+    __shared__ double sm1[kWarps];
+    for (int64_t b = blockIdx.x; b < in.ncols; b += gridDim.x)
+        if (b >= 1)
+            block_totals<1>(in.partial + b * in.ntiles, in.ntiles, in.ntiles, in.rrow + b, sm1, SyncAll());
+}
+
 // ---------------------------------------------------------------------------
 // Column update (deferred step i-1 projection of column i) + norm partials
 // ---------------------------------------------------------------------------
@@ -290,6 +318,7 @@ struct ColArgs {
     const double *r;      // r_{i-1,i} (nullptr: no update)
     const double *xnorm;  // x used for the norm partials when x == nullptr
     NormOut out;          // out.npart == nullptr: update only
+    RrowIn rin;           // deferred r-row totals (rin.partial == nullptr: none)
 };
 
 // Column update (+ norm chains when out.npart): launched with exactly
@@ -301,7 +330,7 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
     pdl_wait();
     if (failed(a.out.status)) return;
     const bool upd = a.r != nullptr;
-    const double rj = upd ? *a.r : 0.0;
+    const double rj = a.rin.partial ? rrow_first(a.rin) : (upd ? *a.r : 0.0);
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x;
     double t = 0.0, zz = 0.0, xx = 0.0;
@@ -336,9 +365,11 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
         }
     }
     pdl_trigger();
-    if (a.out.npart == nullptr) return;  // uniform
-    norm_cta_partial(a.out, t, zz, xx);
-    norm_last_cta(a.out);
+    if (a.out.npart != nullptr) {  // uniform
+        norm_cta_partial(a.out, t, zz, xx);
+        norm_last_cta(a.out);
+    }
+    rrow_rest(a.rin);
 }
 
 // Standalone totals of the norm partials (step API / multi-GPU driver).
@@ -888,6 +919,7 @@ struct CsrArgs {
     const double *r;  // r_{i-1,i}; nullptr: gather X as is
     double *znew;     // updated z_i (own rows)
     NormOut out;      // out.npart == nullptr: plain apply
+    RrowIn rin;       // fused step: deferred r-row totals (partial == nullptr: none)
 };
 
 // sum_q data[q] * xe(indices[q]) over q in [s, e), xe = x - rj qprev (upd)
@@ -1001,13 +1033,13 @@ __global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
     pdl_wait();
     if (failed(a.out.status)) return;
     const bool upd = a.r != nullptr;
-    const double rj = upd ? *a.r : 0.0;
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x;
     double t = 0.0, zz = 0.0, xx = 0.0;
     int64_t row = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     int s = row < a.m ? __ldg(a.indptr + row) : 0;
     int e = row < a.m ? __ldg(a.indptr + row + 1) : 0;
+    const double rj = a.rin.partial ? rrow_first(a.rin) : (upd ? *a.r : 0.0);
     for (int64_t blk = blockIdx.x; blk < nblk; blk += G) {
         const int64_t nrow = row + G * kBlock;  // prefetch the next owned row's pointers
         const int ns = nrow < a.m ? __ldg(a.indptr + nrow) : 0;
@@ -1031,6 +1063,7 @@ __global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
     pdl_trigger();
     norm_cta_partial(a.out, t, zz, xx);
     norm_last_cta(a.out);
+    rrow_rest(a.rin);
 }
 
 // ---------------------------------------------------------------------------
