@@ -125,6 +125,16 @@ AQR_API uint64_t aqr_workspace_bytes(int32_t family, int32_t variant, int32_t or
  * undefined, as the reference raises without a partial result. */
 AQR_API aqr_status aqr_gs_factor(aqr_factor_args *args, void *stream);
 
+/* As aqr_gs_factor, and every column of Q is copied to Q_host (column-major,
+ * leading dimension ldqh; page-locked memory for the copies to overlap) as
+ * soon as it is final -- column i after step i -- on an internal copy
+ * stream, so the device-to-host transfer of Q overlaps the remaining steps;
+ * R goes to R_host (ldrh) at the end.  Returns after all copies completed.
+ * Used by the Python API for page-locked host inputs and by
+ * aqr_gs_factor_host. */
+AQR_API aqr_status aqr_gs_factor_d2h(aqr_factor_args *args, double *Q_host, int64_t ldqh, double *R_host,
+                                     int64_t ldrh, void *stream);
+
 /* Same, with HOST Z/Q/R (column-major, ld = m / m / n) and a host-side
  * operator description (dense A, or CSR with int64 indptr/indices as the
  * reference's CsrSpdOperator holds them, operators.py:100-101).  Owns all

@@ -81,7 +81,7 @@ int sm_count() {
 // host time on the latency-bound small steps).
 template <typename K>
 aqr_status ensure_smem(K kernel, size_t bytes) {
-    if (bytes <= 48 * 1024) return AQR_OK;
+    if (bytes == 0) return AQR_OK;  // (static + dynamic > 48 KB needs the opt-in too)
     static std::mutex mu;
     static std::vector<std::pair<std::pair<const void *, int>, size_t>> done;
     int dev = 0;
@@ -248,6 +248,12 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
             launch_pdl(aqr::csr_step_kernel<8, 4>, g1, aqr::kBlock, 0, s, a);
         else if (sv == 1)
             launch_pdl(aqr::csr_step_kernel<6, 6>, g1, aqr::kBlock, 0, s, a);
+        else if (sv == 5)
+            launch_pdl(aqr::csr_step_kernel<5, 4>, g1, aqr::kBlock, 0, s, a);
+        else if (sv == 6)
+            launch_pdl(aqr::csr_step_kernel<6, 4>, g1, aqr::kBlock, 0, s, a);
+        else if (sv == 7)
+            launch_pdl(aqr::csr_step_kernel<5, 5>, g1, aqr::kBlock, 0, s, a);
         else
             launch_pdl(aqr::csr_step_kernel<8, 1>, g1, aqr::kBlock, 0, s, a);
         timer_end(tix, s);
@@ -614,8 +620,20 @@ T *at(void *base, uint64_t off) {
 
 // ---- the sequencer -------------------------------------------------------------
 
+// Streaming of the finished Q columns to host memory (aqr_gs_factor_d2h):
+// column i is final once step i's launches are enqueued; an event on the
+// compute stream releases its D2H copy on the copy stream, so the transfer
+// of Q overlaps the remaining steps.
+struct HostOut {
+    double *qhost = nullptr;
+    int64_t ldqh = 0;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev = nullptr;
+};
+
 struct Run {
     aqr_factor_args *a;
+    HostOut *ho = nullptr;
     cudaStream_t s;
     bool hp, cgs, naive, csr_native;
     int64_t m, n;
@@ -628,6 +646,16 @@ struct Run {
     bool pending = false;  // row i-1 of R left as trailing partials (RrowIn)
 
     double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
+
+    // Column j of Q is final: stream it to the host (HostOut).
+    aqr_status col_final(int64_t j) {
+        if (!ho || !ho->qhost) return AQR_OK;
+        AQR_CUDA(cudaEventRecord(ho->ev, s));
+        AQR_CUDA(cudaStreamWaitEvent(ho->cs, ho->ev, 0));
+        AQR_CUDA(cudaMemcpyAsync(ho->qhost + j * ho->ldqh, W + j * ldw, 8 * (size_t)m, cudaMemcpyDeviceToHost,
+                                 ho->cs));
+        return AQR_OK;
+    }
 
     aqr::RrowIn rrow_in(int64_t j) const {
         aqr::RrowIn in;
@@ -678,6 +706,12 @@ struct Run {
             // one fused launch: r_{j-1,j} (and the rest of row j-1 of R),
             // gather (z - r q), x = A z, z_new, norm, r_jj
             AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s, pin));
+            static const int rep = [] {  // diagnostics: idempotent repeats of the step
+                const char *e = std::getenv("AQR_SPMV_REPEAT");
+                return e ? std::atoi(e) : 0;
+            }();
+            for (int k = 0; k < rep; ++k)
+                AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s, pin));
             ++mv;
             zcol = zvec;
             xcol = xvec;
@@ -740,6 +774,7 @@ struct Run {
                 const auto h0 = std::chrono::steady_clock::now();
                 const bool can_defer = (hp || csr_native) && i + 1 < n && defer_mode() != 0;
                 AQR_TRY(launch_trailing(t, hp, cgs, s, can_defer ? &pending : nullptr));
+                AQR_TRY(col_final(i));
                 if (dbg) {
                     const auto h1 = std::chrono::steady_clock::now();
                     std::fprintf(stderr, "  step %ld trailing launch host %.1f us, norm-step host %.1f us\n", (long)i,
@@ -796,6 +831,7 @@ struct Run {
             t.qout = col(W, ldw, i);
             t.pout = hp ? pring + (i & 1) * m : nullptr;
             AQR_TRY(launch_trailing(t, hp, cgs, s));  // T_first (vector-only at i = n-1)
+            AQR_TRY(col_final(i));
             if (i + 1 >= n) break;
             AQR_CUDA(cudaEventRecord(e1, s));
             AQR_CUDA(cudaStreamWaitEvent(side, e1, 0));
@@ -837,6 +873,7 @@ struct Run {
             } else {
                 AQR_TRY(launch_normalize(m, zcol, rt(j, j), col(W, ldw, j), xcol, col(P, m, j), status, s));
             }
+            AQR_TRY(col_final(j));
         }
         return AQR_OK;
     }
@@ -919,7 +956,7 @@ aqr_status aqr_status_init(int32_t *status, int64_t n, void *stream) {
     return launched("status_init_kernel");
 }
 
-aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
+static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho) {
     if (!a) return set_err(AQR_EARG, "null args");
     a->fail_col = -1;
     a->fail_val = 0.0;
@@ -939,6 +976,7 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
 
     Run r;
     r.a = a;
+    r.ho = ho;
     r.s = S(stream);
     r.hp = a->variant == AQR_HP;
     r.naive = a->variant == AQR_NAIVE;
@@ -1010,6 +1048,30 @@ aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) {
         return set_err(AQR_EBREAKDOWN, "breakdown at column " + std::to_string(st[0]));
     }
     return AQR_OK;
+}
+
+aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) { return gs_factor_impl(a, stream, nullptr); }
+
+aqr_status aqr_gs_factor_d2h(aqr_factor_args *a, double *Q_host, int64_t ldqh, double *R_host, int64_t ldrh,
+                             void *stream) {
+    if (!a || !Q_host || !R_host) return set_err(AQR_EARG, "null args / host buffers");
+    if (ldqh < a->m || ldrh < a->n) return set_err(AQR_EARG, "bad host leading dimension");
+    SideCtx sc;
+    AQR_TRY(side_acquire(sc));
+    HostOut ho;
+    ho.qhost = Q_host;
+    ho.ldqh = ldqh;
+    ho.cs = sc.side;
+    ho.ev = sc.e1;
+    aqr_status st = gs_factor_impl(a, stream, &ho);  // returns after the compute stream drained
+    if (st == AQR_OK &&
+        cudaMemcpy2DAsync(R_host, 8 * (size_t)ldrh, a->R, 8 * (size_t)a->ldr, 8 * (size_t)a->n, (size_t)a->n,
+                          cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess)
+        st = set_err(AQR_ECUDA, "D2H R");
+    if (cudaStreamSynchronize(sc.side) != cudaSuccess && st == AQR_OK) st = set_err(AQR_ECUDA, "D2H Q");
+    if (cudaStreamSynchronize(S(stream)) != cudaSuccess && st == AQR_OK) st = set_err(AQR_ECUDA, "D2H R");
+    side_release(sc);
+    return st;
 }
 
 aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientation, int64_t m,
@@ -1093,16 +1155,10 @@ aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientati
         a.workspace = ws;
         a.workspace_bytes = wsb;
         a.flagged_host = flagged_host;
-        st = aqr_gs_factor(&a, s);
+        st = aqr_gs_factor_d2h(&a, Q_host, m, R_host, n, s);  // Q streamed as columns finish
         if (fail_col) *fail_col = a.fail_col;
         if (fail_val) *fail_val = a.fail_val;
         if (mv_count) *mv_count = a.mv_count;
-    }
-    if (st == AQR_OK) {
-        if (cudaMemcpyAsync(Q_host, Q, 8 * (size_t)m * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaMemcpyAsync(R_host, R, 8 * (size_t)n * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-            cudaStreamSynchronize(s) != cudaSuccess)
-            st = set_err(AQR_ECUDA, "D2H Q/R");
     }
     cleanup();
     return st;

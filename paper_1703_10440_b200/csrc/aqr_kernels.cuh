@@ -209,13 +209,16 @@ __device__ __forceinline__ void norm_finish_dev(int64_t i, double t, double zz, 
     *rii = sqrt(t);                                               // gram_schmidt.py:159
 }
 
-// Block-wide "am I the last CTA" ticket (all kBlock threads call it after
-// writing their partials).  Resets the counter when it fires.
+// Block-wide "am I the last CTA" ticket (all kBlock threads call it; the
+// CTA's partials were written by thread 0, which alone fences before taking
+// the ticket -- the other warps retire without waiting for their stores).
+// Resets the counter when it fires.
 __device__ __forceinline__ bool last_block(unsigned *counter, unsigned expected) {
     __shared__ unsigned ticket;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) ticket = atomicAdd(counter, 1u);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        ticket = atomicAdd(counter, 1u);
+    }
     __syncthreads();
     const bool last = ticket == expected - 1;
     if (last) {
@@ -239,7 +242,8 @@ struct NormOut {
 
 // Norm partial of this CTA (all kBlock threads call it once, with their
 // accumulated chains): block tree, then partial blockIdx.x of each term.
-__device__ __forceinline__ void norm_cta_partial(const NormOut &o, double t, double zz, double xx) {
+__device__ __forceinline__ void norm_cta_partial(const NormOut &o, double t, double zz, double xx,
+                                                 int64_t cta) {
     __shared__ double sm[3 * kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     t = warp_sum(t);
@@ -251,20 +255,23 @@ __device__ __forceinline__ void norm_cta_partial(const NormOut &o, double t, dou
         sm[2 * kWarps + warp] = xx;
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
-        double s = sm[threadIdx.x * kWarps];
+    if (threadIdx.x == 0) {  // thread 0 writes all three (see last_block)
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, sm[threadIdx.x * kWarps + w]);
-        o.npart[(int64_t)threadIdx.x * o.ntiles + blockIdx.x] = s;
+        for (int c = 0; c < 3; ++c) {
+            double s = sm[c * kWarps];
+#pragma unroll
+            for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, sm[c * kWarps + w]);
+            o.npart[(int64_t)c * o.ntiles + cta] = s;
+        }
     }
 }
 
 // After a CTA wrote all its tiles' partials: the last CTA of the grid forms
 // the totals (block_totals) and finishes the column (one ticket per CTA).
 // Called by all kBlock threads.
-__device__ __forceinline__ void norm_last_cta(const NormOut &o) {
+__device__ __forceinline__ void norm_last_cta(const NormOut &o, unsigned ctas) {
     if (o.counter == nullptr) return;
-    if (!last_block(o.counter, gridDim.x)) return;
+    if (!last_block(o.counter, ctas)) return;
     __shared__ double tot[3];
     __shared__ double sm3[3 * kWarps];
     block_totals<3>(o.npart, o.ntiles, o.ntiles, tot, sm3, SyncAll());
@@ -289,19 +296,20 @@ struct RrowIn {
     double *rrow;  // rrow[b] = Rt[i-1][i+b]
 };
 
-__device__ __forceinline__ double rrow_first(const RrowIn &in) {
+__device__ __forceinline__ double rrow_first(const RrowIn &in, bool writer) {
     __shared__ double tot1[1];
     __shared__ double sm1[kWarps];
     block_totals<1>(in.partial, in.ntiles, in.ntiles, tot1, sm1, SyncAll());
     const double r = tot1[0];
-    if (blockIdx.x == 0 && threadIdx.x == 0) in.rrow[0] = r;
+    if (writer && threadIdx.x == 0) in.rrow[0] = r;
     return r;
 }
 
-__device__ __forceinline__ void rrow_rest(const RrowIn &in) {
+// CTA `cta` of `G` reduces columns cta, cta + G, ... (column 0 excluded).
+__device__ __forceinline__ void rrow_rest(const RrowIn &in, int64_t cta, int64_t G) {
     if (in.partial == nullptr) return;
     __shared__ double sm1[kWarps];
-    for (int64_t b = blockIdx.x; b < in.ncols; b += gridDim.x)
+    for (int64_t b = cta; b < in.ncols; b += G)
         if (b >= 1)
             block_totals<1>(in.partial + b * in.ntiles, in.ntiles, in.ntiles, in.rrow + b, sm1, SyncAll());
 }
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
     pdl_wait();
     if (failed(a.out.status)) return;
     const bool upd = a.r != nullptr;
-    const double rj = a.rin.partial ? rrow_first(a.rin) : (upd ? *a.r : 0.0);
+    const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x;
     double t = 0.0, zz = 0.0, xx = 0.0;
@@ -366,10 +374,10 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
     }
     pdl_trigger();
     if (a.out.npart != nullptr) {  // uniform
-        norm_cta_partial(a.out, t, zz, xx);
-        norm_last_cta(a.out);
+        norm_cta_partial(a.out, t, zz, xx, blockIdx.x);
+        norm_last_cta(a.out, gridDim.x);
     }
-    rrow_rest(a.rin);
+    rrow_rest(a.rin, blockIdx.x, gridDim.x);
 }
 
 // Standalone totals of the norm partials (step API / multi-GPU driver).
@@ -495,20 +503,17 @@ __device__ __forceinline__ void trail_vectors(const TrailArgs &a, int64_t row0, 
     }
 }
 
+// One (tile, column group) work unit of the trailing pass (all kBlock threads).
 template <int RPT, int CU, bool HP, bool CGS>
-__global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
-    pdl_wait();
-    if (failed(a.status)) return;
-    extern __shared__ double wsum[];  // [kWarps][cpg]
-    const int tile = blockIdx.x;
+__device__ __forceinline__ void trail_body(const TrailArgs &a, int tile, int group, double *wsum) {
     const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
-    const int cbeg = a.jbeg + blockIdx.y * a.cpg;
+    const int cbeg = a.jbeg + group * a.cpg;
     const int cend = min(a.jend, cbeg + a.cpg);
     const bool upd = a.qprev != nullptr;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     double q[RPT], p[RPT], pp[RPT];
-    trail_vectors<RPT, HP>(a, row0, blockIdx.y == 0, q, p, pp);
+    trail_vectors<RPT, HP>(a, row0, group == 0, q, p, pp);
     bool ok[RPT];
 #pragma unroll
     for (int u = 0; u < RPT; ++u) ok[u] = row0 + (int64_t)u * kBlock < a.m;
@@ -564,7 +569,15 @@ __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
         for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsum[w * a.cpg + c]);
         a.partial[(int64_t)(cbeg - a.jbeg + c) * a.ntiles + tile] = s;
     }
-    // totals: rrow_reduce_kernel (one CTA per column) follows this launch
+}
+
+template <int RPT, int CU, bool HP, bool CGS>
+__global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
+    pdl_wait();
+    if (failed(a.status)) return;
+    extern __shared__ double wsum[];  // [kWarps][cpg]
+    trail_body<RPT, CU, HP, CGS>(a, blockIdx.x, blockIdx.y, wsum);
+    // totals: the next step's norm kernel (RrowIn) or rrow_reduce_kernel
 }
 
 // ---------------------------------------------------------------------------
@@ -1024,23 +1037,18 @@ __global__ void __launch_bounds__(kBlock) csr_row_kernel(CsrArgs a) {
     }
 }
 
-// Fused HA/naive step, launched with exactly norm_tiles(m) CTAs (the
-// canonical norm grid): CTA b handles rows of the 256-row blocks b, b+G, ...
-// one per thread, accumulating the norm chains in ascending block order; the
-// next row's pointers are prefetched; one block tree per CTA at the end.
-template <int B, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
-    pdl_wait();
-    if (failed(a.out.status)) return;
+// The fused step of virtual CTA `cta` of the canonical norm grid G (called by
+// all kBlock threads of a CTA).
+template <int B>
+__device__ __forceinline__ void csr_step_body(const CsrArgs &a, int64_t cta, int64_t G) {
     const bool upd = a.r != nullptr;
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
-    const int64_t G = gridDim.x;
     double t = 0.0, zz = 0.0, xx = 0.0;
-    int64_t row = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    int64_t row = cta * kBlock + threadIdx.x;
     int s = row < a.m ? __ldg(a.indptr + row) : 0;
     int e = row < a.m ? __ldg(a.indptr + row + 1) : 0;
-    const double rj = a.rin.partial ? rrow_first(a.rin) : (upd ? *a.r : 0.0);
-    for (int64_t blk = blockIdx.x; blk < nblk; blk += G) {
+    const double rj = a.rin.partial ? rrow_first(a.rin, cta == 0) : (upd ? *a.r : 0.0);
+    for (int64_t blk = cta; blk < nblk; blk += G) {
         const int64_t nrow = row + G * kBlock;  // prefetch the next owned row's pointers
         const int ns = nrow < a.m ? __ldg(a.indptr + nrow) : 0;
         const int ne = nrow < a.m ? __ldg(a.indptr + nrow + 1) : 0;
@@ -1061,9 +1069,20 @@ __global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
         e = ne;
     }
     pdl_trigger();
-    norm_cta_partial(a.out, t, zz, xx);
-    norm_last_cta(a.out);
-    rrow_rest(a.rin);
+    norm_cta_partial(a.out, t, zz, xx, cta);
+    norm_last_cta(a.out, (unsigned)G);
+}
+
+// Fused HA/naive step, launched with exactly norm_tiles(m) CTAs (the
+// canonical norm grid): CTA b handles rows of the 256-row blocks b, b+G, ...
+// one per thread, accumulating the norm chains in ascending block order; the
+// next row's pointers are prefetched; one block tree per CTA at the end.
+template <int B, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
+    pdl_wait();
+    if (failed(a.out.status)) return;
+    csr_step_body<B>(a, blockIdx.x, gridDim.x);
+    rrow_rest(a.rin, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -201,7 +201,15 @@ def _gs_factor(Z, op, family, variant, orientation):
     a.op = ctypes.pointer(desc)
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     a.flagged_host = flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    status = L.aqr_gs_factor(ctypes.byref(a), D.stream_ptr())
+    if D.is_torch(Z) and not Z.is_cuda and Z.is_pinned():
+        # page-locked host input: Q columns stream back to page-locked host
+        # memory while the later steps run (aqr_gs_factor_d2h)
+        Qh = t.empty((n, m), dtype=t.float64, pin_memory=True).t()
+        Rh = t.empty((n, n), dtype=t.float64, pin_memory=True).t()
+        status = L.aqr_gs_factor_d2h(ctypes.byref(a), Qh.data_ptr(), m, Rh.data_ptr(), n, D.stream_ptr())
+        back = lambda T: Qh if T is Q else Rh  # noqa: E731
+    else:
+        status = L.aqr_gs_factor(ctypes.byref(a), D.stream_ptr())
     if cb is not None and cb.error is not None:
         raise cb.error
     fail_col = int(a.fail_col) if status == _lib.AQR_EBREAKDOWN else None

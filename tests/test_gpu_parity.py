@@ -264,3 +264,54 @@ def test_operator_counts_and_errors(aqr):
         op.apply([1.0, 2.0])
     with pytest.raises(aqr.DimensionError):
         op.apply_block(np.ones((2, 2)))
+
+
+@pytest.mark.parametrize("meth", ["mgs-ha-row", "mgs-hp-row", "mgs-naive-col"])
+def test_pinned_host_input_streams_q_bitwise(aqr, meth):
+    """Page-locked host Z: Q columns stream back while later steps run
+    (aqr_gs_factor_d2h); results equal the device-resident call bitwise."""
+    import torch
+
+    from paper_1703_10440_b200 import problems
+
+    ip, ix, dv = problems.laplacian5(640, 480, 1e-2)  # m = 307200: the RPT = 8 tiles
+    m, n = 640 * 480, 10
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    Z = problems.rng(9, 0).standard_normal((n, m)).T
+    Zh = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
+    Zh.copy_(torch.from_numpy(Z))
+    rd = aqr.factorize(Zh.cuda(), op, meth)
+    rh = aqr.factorize(Zh, op, meth)
+    assert not rh.Q.is_cuda and rh.Q.is_pinned() and not rh.R.is_cuda
+    assert torch.equal(rh.Q, rd.Q.cpu()) and torch.equal(rh.R, rd.R.cpu())
+    assert rh.cost.mv_count == rd.cost.mv_count
+
+
+def test_host_c_entry_matches_device_path(aqr):
+    """aqr_gs_factor_host (numpy buffers, int64 CSR)."""
+    import ctypes
+
+    from paper_1703_10440_b200 import _lib, problems
+
+    ip, ix, dv = problems.laplacian5(96, 80, 1e-2)
+    m, n = 96 * 80, 9
+    Z = np.asfortranarray(problems.rng(9, 1).standard_normal((m, n)))
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    L = _lib.lib()
+    ip64, ix64 = np.ascontiguousarray(ip, dtype=np.int64), np.ascontiguousarray(ix, dtype=np.int64)
+    dv64 = np.ascontiguousarray(dv, dtype=np.float64)
+    d, i64 = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+    for fam, var, ori, meth in ((0, 1, 1, "mgs-ha-row"), (0, 2, 1, "mgs-hp-row"), (1, 0, 0, "cgs-naive-col")):
+        Q = np.empty((m, n), order="F")
+        R = np.empty((n, n), order="F")
+        flags = np.zeros(n, dtype=np.int32)
+        fail, fval, mv = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()
+        st = L.aqr_gs_factor_host(fam, var, ori, m, n, Z.ctypes.data_as(d), Q.ctypes.data_as(d),
+                                  R.ctypes.data_as(d), 1, None, ip64.ctypes.data_as(i64),
+                                  ix64.ctypes.data_as(i64), dv64.ctypes.data_as(d), int(ix64.size),
+                                  ctypes.byref(fail), ctypes.byref(fval),
+                                  flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(mv))
+        assert st == 0, L.aqr_last_error()
+        r = aqr.factorize(Z, op, meth)
+        assert np.array_equal(Q, r.Q) and np.array_equal(R, r.R), meth
+        assert mv.value == r.cost.mv_count

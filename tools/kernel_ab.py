@@ -23,7 +23,7 @@ for _ in range(K):
     aqr.factorize(Zd, op, meth)
 torch.cuda.synchronize()
 out = {"variant": os.environ.get("AQR_TRAIL_VARIANT", "0"), "method": meth, "step_ms": step}
-for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update")):
+for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update"), (3, "spmv_trail")):
     n, ms, b = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
     L.aqr_kernel_timer_read(slot, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b))
     if n.value:
