@@ -76,8 +76,45 @@ def to_device_f(a, dev=None):
             ld = leading_dim(T)
         return T, ld
     A = np.asfortranarray(a, dtype=np.float64)
+    if A.ndim == 2 and A.nbytes >= _STAGE_MIN_BYTES:
+        return _h2d_staged(A, dev), max(A.shape[0], 1)
     T = t.from_numpy(A.T.copy(order="C") if not A.flags.f_contiguous else A.T).to(dev).t()
     return T, max(A.shape[0], 1)
+
+
+# Large numpy inputs: a pageable host->device copy runs at ~11 GB/s through
+# the driver's staging buffers.  Instead, host threads copy column chunks into
+# a page-locked staging block (numpy releases the GIL) and each chunk's DMA is
+# queued on the current stream as soon as its copy is done (~55 GB/s).  The
+# staging block comes from torch's page-locked cache, which keeps it alive
+# until the queued copies complete.
+_STAGE_MIN_BYTES = 64 << 20
+_STAGE_THREADS = 8
+_pool = None
+
+
+def _h2d_staged(A, dev):
+    global _pool
+    t = torch()
+    m, n = A.shape
+    if _pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="aqr-h2d")
+    out = t.empty((n, m), dtype=t.float64, device=dev)  # row j = column j (column-major (m, n))
+    stage = t.empty((n, m), dtype=t.float64, pin_memory=True)
+    src, dst = A.T, stage.numpy()  # (n, m) C-ordered views
+    nchunks = min(n, 4 * _STAGE_THREADS)
+    bounds = [(k * n) // nchunks for k in range(nchunks + 1)]
+    futs = [_pool.submit(np.copyto, dst[b0:b1], src[b0:b1]) for b0, b1 in zip(bounds[:-1], bounds[1:]) if b1 > b0]
+    k = 0
+    for b0, b1 in zip(bounds[:-1], bounds[1:]):
+        if b1 <= b0:
+            continue
+        futs[k].result()
+        k += 1
+        out[b0:b1].copy_(stage[b0:b1], non_blocking=True)
+    return out.t()
 
 
 class CudaArray:

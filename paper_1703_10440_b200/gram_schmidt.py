@@ -201,13 +201,18 @@ def _gs_factor(Z, op, family, variant, orientation):
     a.op = ctypes.pointer(desc)
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     a.flagged_host = flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    if D.is_torch(Z) and not Z.is_cuda and Z.is_pinned():
-        # page-locked host input: Q columns stream back to page-locked host
-        # memory while the later steps run (aqr_gs_factor_d2h)
+    if not (D.is_torch(Z) and Z.is_cuda):
+        # host input (numpy or CPU tensor): Q columns stream back into
+        # page-locked host memory while the later steps run
+        # (aqr_gs_factor_d2h); numpy callers get F-ordered views of it (the
+        # page-locked block returns to torch's host cache when they drop it)
         Qh = t.empty((n, m), dtype=t.float64, pin_memory=True).t()
         Rh = t.empty((n, n), dtype=t.float64, pin_memory=True).t()
         status = L.aqr_gs_factor_d2h(ctypes.byref(a), Qh.data_ptr(), m, Rh.data_ptr(), n, D.stream_ptr())
-        back = lambda T: Qh if T is Q else Rh  # noqa: E731
+        if D.is_torch(Z):
+            back = lambda T: Qh if T is Q else Rh  # noqa: E731
+        else:
+            back = lambda T: (Qh if T is Q else Rh).numpy()  # noqa: E731
     else:
         status = L.aqr_gs_factor(ctypes.byref(a), D.stream_ptr())
     if cb is not None and cb.error is not None:

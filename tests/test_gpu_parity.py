@@ -315,3 +315,23 @@ def test_host_c_entry_matches_device_path(aqr):
         r = aqr.factorize(Z, op, meth)
         assert np.array_equal(Q, r.Q) and np.array_equal(R, r.R), meth
         assert mv.value == r.cost.mv_count
+
+
+def test_large_numpy_input_staged_h2d_bitwise(aqr):
+    """numpy in / numpy out above the staging threshold (threaded page-locked
+    H2D staging, streamed D2H): same bits as the device-resident call."""
+    import torch
+
+    from paper_1703_10440_b200 import _device, problems
+
+    ip, ix, dv = problems.laplacian5(1024, 1024, 1e-2)
+    m, n = 1024 * 1024, 9
+    assert 8 * m * n >= _device._STAGE_MIN_BYTES
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    Z = np.asfortranarray(problems.rng(9, 2).standard_normal((m, n)))
+    Z0 = Z.copy(order="F")
+    r = aqr.mgs_ha(Z, op, "row")
+    rd = aqr.mgs_ha(torch.from_numpy(Z.T).cuda().t(), op, "row")
+    assert isinstance(r.Q, np.ndarray) and r.Q.flags.f_contiguous and r.Q.shape == (m, n)
+    assert np.array_equal(r.Q, rd.Q.cpu().numpy()) and np.array_equal(r.R, rd.R.cpu().numpy())
+    assert np.array_equal(Z, Z0)
