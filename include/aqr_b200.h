@@ -75,7 +75,7 @@ typedef int (*aqr_apply_fn)(void *ctx, int64_t k, const double *X, int64_t ldx, 
 
 typedef struct aqr_op {
     int32_t kind; /* aqr_op_kind */
-    int32_t spmv_lanes; /* CSR: lanes cooperating on one row (1..32, 0 = auto) */
+    int32_t max_row_nnz; /* CSR: longest row (0 = unknown); picks the SpMV row batch, results unchanged */
     int64_t m;
     /* AQR_OP_DENSE */
     const double *A;

@@ -34,16 +34,19 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in DEPENDS)
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Build OUT (or `out` with extra -D `defines`, for tools/ A/B variants)."""
+    if out is None and not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-o", OUT + ".tmp", *SOURCES]
+    target = out or OUT
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(REPO, "include"),
+           "-o", target + ".tmp", *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

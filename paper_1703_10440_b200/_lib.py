@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaqr_b200.so")
+# AQR_LIB_PATH: an alternative build of the same library (tools/ A/B experiments)
+LIB_PATH = os.environ.get("AQR_LIB_PATH") or os.path.join(_HERE, "libaqr_b200.so")
 ABI_VERSION = 1
 
 AQR_OK, AQR_EDIM, AQR_EBREAKDOWN, AQR_ECUDA, AQR_EARG, AQR_ENOMEM, AQR_ECALLBACK = range(7)
@@ -36,7 +37,7 @@ APPLY_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
 
 class AqrOp(ctypes.Structure):
     _fields_ = [
-        ("kind", c_i32), ("spmv_lanes", c_i32), ("m", c_i64),
+        ("kind", c_i32), ("max_row_nnz", c_i32), ("m", c_i64),
         ("A", c_vp), ("lda", c_i64),
         ("indptr", c_vp), ("indices", c_vp), ("data", c_vp), ("nnz", c_i64),
         ("apply", APPLY_FN), ("apply_block", APPLY_FN), ("ctx", c_vp),

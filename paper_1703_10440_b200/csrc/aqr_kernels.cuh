@@ -52,7 +52,10 @@ __host__ __device__ inline int64_t num_tiles(int64_t m) {
 // block in ascending block order; one block tree (warp xor butterfly, warps
 // ascending) per CTA gives partial b.  No barrier inside the row loop, one
 // per CTA at the end.  Totals are block_totals over the G partials.
-constexpr int kNormGrid = 148 * 8;
+#ifndef AQR_NORM_GRID
+#define AQR_NORM_GRID (148 * 4)
+#endif
+constexpr int kNormGrid = AQR_NORM_GRID;
 __host__ __device__ inline int64_t norm_tiles(int64_t m) {
     const int64_t b = (m + kBlock - 1) / kBlock;
     return b < kNormGrid ? b : kNormGrid;
@@ -935,26 +938,28 @@ struct CsrArgs {
     RrowIn rin;       // fused step: deferred r-row totals (partial == nullptr: none)
 };
 
-// sum_q data[q] * xe(indices[q]) over q in [s, e), xe = x - rj qprev (upd)
+// sum_q data[q] * xe(indices[q]) over q in [s, e), xe = x - rj qprev (upd),
+// in batches of B entries (loads of a batch in flight together)
+template <int B = kRowBatch>
 __device__ __forceinline__ double csr_row(const CsrArgs &a, const double *x, int s, int e,
                                           bool upd, double rj) {
     double acc = 0.0;
-    for (int q0 = s; q0 < e; q0 += kRowBatch) {
-        int c[kRowBatch];
-        double v[kRowBatch], xv[kRowBatch];
+    for (int q0 = s; q0 < e; q0 += B) {
+        int c[B];
+        double v[B], xv[B];
 #pragma unroll
-        for (int h = 0; h < kRowBatch; ++h) {
+        for (int h = 0; h < B; ++h) {
             const bool ok = q0 + h < e;
             c[h] = ok ? __ldg(a.indices + q0 + h) : 0;
             v[h] = ok ? __ldg(a.data + q0 + h) : 0.0;
         }
 #pragma unroll
-        for (int h = 0; h < kRowBatch; ++h) {
+        for (int h = 0; h < B; ++h) {
             xv[h] = q0 + h < e ? __ldg(x + c[h]) : 0.0;
             if (upd && q0 + h < e) xv[h] = __dsub_rn(xv[h], __dmul_rn(rj, __ldg(a.qprev + c[h])));
         }
 #pragma unroll
-        for (int h = 0; h < kRowBatch; ++h)
+        for (int h = 0; h < B; ++h)
             if (q0 + h < e) acc = __dadd_rn(acc, __dmul_rn(v[h], xv[h]));
     }
     return acc;
@@ -971,7 +976,7 @@ __device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], co
     for (int i = 0; i < R; ++i) short_rows &= (e[i] - s[i] <= B);
     if (!short_rows) {
 #pragma unroll
-        for (int i = 0; i < R; ++i) y[i] = csr_row(a, a.X, s[i], e[i], upd, rj);
+        for (int i = 0; i < R; ++i) y[i] = csr_row<B>(a, a.X, s[i], e[i], upd, rj);
         return;
     }
     int c[R][B];

@@ -174,6 +174,7 @@ class DistCsrSpdOperator(SpdOperator):
             d.m = self.dim
             d.indptr, d.indices, d.data = (a.data_ptr() for a in self._dev)
             d.nnz = self.nnz
+            d.max_row_nnz = int(np.diff(self.indptr).max()) if self.dim else 0
             self._desc = d
         return self._desc
 

@@ -176,11 +176,12 @@ class CsrSpdOperator(SpdOperator):
 
     ``indptr``/``indices``/``data`` may be numpy arrays (validated exactly as
     the reference does, int64 host copies kept) or CUDA tensors (validated on
-    the device, used for inputs generated on the GPU).  ``spmv_lanes``: lanes
-    cooperating on one row in the SpMV/SpMM kernels (0 = chosen from nnz/m).
+    the device, used for inputs generated on the GPU).  ``max_row_nnz``: the
+    longest row, measured here when not given; it only selects the SpMV
+    kernel's row batch (results are identical for every value).
     """
 
-    def __init__(self, indptr, indices, data, dim=None, spmv_lanes=0):
+    def __init__(self, indptr, indices, data, dim=None, max_row_nnz=None):
         if D.is_torch(indptr):
             self._init_device(indptr, indices, data, dim)
         else:
@@ -199,7 +200,13 @@ class CsrSpdOperator(SpdOperator):
             super().__init__(m)
             self.indptr, self.indices, self.data = indptr, indices, data
             self._dev = None
-        self.spmv_lanes = int(spmv_lanes)
+        if max_row_nnz is None:
+            if D.is_torch(self.indptr):
+                d = self.indptr[1:] - self.indptr[:-1]
+                max_row_nnz = int(d.max()) if d.numel() else 0
+            else:
+                max_row_nnz = int(np.diff(self.indptr).max()) if self.dim else 0
+        self.max_row_nnz = int(max_row_nnz)
         self._desc = None
 
     def _init_device(self, indptr, indices, data, dim):
@@ -239,7 +246,7 @@ class CsrSpdOperator(SpdOperator):
             ip, ix, dv, _ = self._device_arrays()
             d = _lib.AqrOp()
             d.kind = _lib.AQR_OP_CSR
-            d.spmv_lanes = self.spmv_lanes
+            d.max_row_nnz = min(self.max_row_nnz, 2**31 - 1)
             d.m = self.dim
             d.indptr, d.indices, d.data = ip.data_ptr(), ix.data_ptr(), dv.data_ptr()
             d.nnz = self.nnz
