@@ -258,7 +258,15 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         timer_end(tix, s);
         return launched("csr_step_kernel");
     }
-    aqr::csr_row_kernel<<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    const int32_t mr = op->max_row_nnz;
+    if (mr >= 1 && mr <= 4)
+        aqr::csr_row_kernel<4><<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    else if (mr == 5)
+        aqr::csr_row_kernel<5><<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    else if (mr == 6)
+        aqr::csr_row_kernel<6><<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
+    else
+        aqr::csr_row_kernel<8><<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
     return launched("csr_row_kernel");
 }
 

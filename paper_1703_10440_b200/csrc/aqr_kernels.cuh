@@ -1008,6 +1008,7 @@ __device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], co
 }
 
 // Plain apply, k >= 1 columns: grid-stride over 256-row blocks.
+template <int B>
 __global__ void __launch_bounds__(kBlock) csr_row_kernel(CsrArgs a) {
     const int64_t nblocks = (a.m + kBlock - 1) / kBlock;
     for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
@@ -1015,29 +1016,30 @@ __global__ void __launch_bounds__(kBlock) csr_row_kernel(CsrArgs a) {
         if (row >= a.m) continue;
         const int s = __ldg(a.indptr + row);
         const int e = __ldg(a.indptr + row + 1);
-        if (e - s <= kRowBatch && a.k > 1) {  // entries stay in registers across columns
-            int c[kRowBatch];
-            double val[kRowBatch];
+        if (e - s <= B && a.k > 1) {  // entries stay in registers across columns
+            int c[B];
+            double val[B];
 #pragma unroll
-            for (int h = 0; h < kRowBatch; ++h) {
+            for (int h = 0; h < B; ++h) {
                 const bool ok = s + h < e;
                 c[h] = ok ? __ldg(a.indices + s + h) : 0;
                 val[h] = ok ? __ldg(a.data + s + h) : 0.0;
             }
+#pragma unroll 2
             for (int64_t col = 0; col < a.k; ++col) {
                 const double *x = a.X + col * a.ldx;
-                double xv[kRowBatch];
+                double xv[B];
 #pragma unroll
-                for (int h = 0; h < kRowBatch; ++h) xv[h] = s + h < e ? __ldg(x + c[h]) : 0.0;
+                for (int h = 0; h < B; ++h) xv[h] = s + h < e ? __ldg(x + c[h]) : 0.0;
                 double acc = 0.0;
 #pragma unroll
-                for (int h = 0; h < kRowBatch; ++h)
+                for (int h = 0; h < B; ++h)
                     if (s + h < e) acc = __dadd_rn(acc, __dmul_rn(val[h], xv[h]));
                 a.Y[row + col * a.ldy] = acc;
             }
         } else {
             for (int64_t col = 0; col < a.k; ++col)
-                a.Y[row + col * a.ldy] = csr_row(a, a.X + col * a.ldx, s, e, false, 0.0);
+                a.Y[row + col * a.ldy] = csr_row<B>(a, a.X + col * a.ldx, s, e, false, 0.0);
         }
     }
 }
