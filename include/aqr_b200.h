@@ -135,6 +135,19 @@ AQR_API aqr_status aqr_gs_factor(aqr_factor_args *args, void *stream);
 AQR_API aqr_status aqr_gs_factor_d2h(aqr_factor_args *args, double *Q_host, int64_t ldqh, double *R_host,
                                      int64_t ldrh, void *stream);
 
+/* Host Z in, host Q / R out, with both transfers overlapped with the
+ * factorization (row orientation): Z is copied in chunks of `chunk_cols`
+ * columns (0 = n/8) on an internal stream; the step loop brings a chunk in
+ * when it needs it, after replaying the steps already done on it (the same
+ * trailing passes and reduction trees: results are bitwise those of
+ * aqr_gs_factor), and Q columns stream out as in aqr_gs_factor_d2h.  args->Q
+ * is the device working matrix (Z is staged into it; args->Z is ignored);
+ * Z_host / Q_host should be page-locked.  The column form copies Z in whole,
+ * then runs aqr_gs_factor_d2h.  Returns after all copies completed. */
+AQR_API aqr_status aqr_gs_factor_pinned(aqr_factor_args *args, const double *Z_host, int64_t ldzh,
+                                        double *Q_host, int64_t ldqh, double *R_host, int64_t ldrh,
+                                        int64_t chunk_cols, void *stream);
+
 /* Same, with HOST Z/Q/R (column-major, ld = m / m / n) and a host-side
  * operator description (dense A, or CSR with int64 indptr/indices as the
  * reference's CsrSpdOperator holds them, operators.py:100-101).  Owns all

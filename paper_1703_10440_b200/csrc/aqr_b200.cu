@@ -498,7 +498,8 @@ aqr_status side_acquire(SideCtx &c) {
     int lo = 0, hi = 0;
     AQR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     c.dev = dev;
-    AQR_CUDA(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, hi));
+    (void)hi;
+    AQR_CUDA(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, lo));  // copy streams
     AQR_CUDA(cudaEventCreateWithFlags(&c.e1, cudaEventDisableTiming));
     AQR_CUDA(cudaEventCreateWithFlags(&c.e2, cudaEventDisableTiming));
     return AQR_OK;
@@ -517,71 +518,16 @@ int defer_mode() {  // AQR_DEFER=0: separate r-row reduction launch (A/B experim
     return v;
 }
 
-int lookahead_mode() {  // AQR_LOOKAHEAD=0 disables (A/B experiments)
-    static const int v = [] {
-        const char *e = std::getenv("AQR_LOOKAHEAD");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
 
-// ---- L2 residency of the operator --------------------------------------------
-// The CSR operator (values, indices, row pointers: 12 nnz + 4 m bytes, 67 MB
-// at config 2) is re-read by every step's SpMV while the trailing pass
-// streams ~1 GB per step through the 126 MB L2 (with evict-first hints).
-// When the three arrays are adjacent in memory (the Python operator
-// allocates them in one block), a persisting access-policy window on the
-// stream keeps them L2-resident for the whole factorization.
-struct L2Window {
-    bool active = false;
-    cudaStream_t s = nullptr;
-};
-
-int l2_persist_mode() {  // AQR_L2_PERSIST=0 disables (A/B experiments)
-    static const int v = [] {
-        const char *e = std::getenv("AQR_L2_PERSIST");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-aqr_status l2_window_begin(const aqr_op *op, cudaStream_t s, L2Window &w) {
-    if (l2_persist_mode() == 0 || op->kind != AQR_OP_CSR || op->nnz <= 0) return AQR_OK;
-    const uintptr_t p0 = (uintptr_t)op->data, p1 = (uintptr_t)op->indices, p2 = (uintptr_t)op->indptr;
-    const uintptr_t lo = std::min(p0, std::min(p1, p2));
-    const uintptr_t hi = std::max(p0 + 8 * (uintptr_t)op->nnz,
-                                  std::max(p1 + 4 * (uintptr_t)op->nnz, p2 + 4 * (uintptr_t)(op->m + 1)));
-    const size_t need = 12 * (size_t)op->nnz + 4 * (size_t)(op->m + 1);
-    if (hi - lo > need + need / 8) return AQR_OK;  // not one block: leave the cache alone
-    int dev = 0, max_win = 0, max_persist = 0;
-    AQR_CUDA(cudaGetDevice(&dev));
-    AQR_CUDA(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-    AQR_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
-    if (max_win <= 0 || max_persist <= 0) return AQR_OK;
-    const size_t bytes = std::min<size_t>(hi - lo, (size_t)max_win);
-    const size_t persist = std::min<size_t>(bytes, (size_t)max_persist);
-    AQR_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-    cudaStreamAttrValue attr;
-    std::memset(&attr, 0, sizeof attr);
-    attr.accessPolicyWindow.base_ptr = reinterpret_cast<void *>(lo);
-    attr.accessPolicyWindow.num_bytes = bytes;
-    attr.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)bytes);
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    AQR_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr));
-    w.active = true;
-    w.s = s;
-    return AQR_OK;
-}
-
-void l2_window_end(L2Window &w) {
-    if (!w.active) return;
-    cudaStreamAttrValue attr;
-    std::memset(&attr, 0, sizeof attr);
-    attr.accessPolicyWindow.num_bytes = 0;
-    cudaStreamSetAttribute(w.s, cudaStreamAttributeAccessPolicyWindow, &attr);
-    cudaCtxResetPersistingL2Cache();
-    w.active = false;
+// Column-block copy (rows x cols doubles, leading dimensions in elements):
+// one linear cudaMemcpyAsync when both sides are contiguous (the DMA engines'
+// fast path), else a pitched copy.
+cudaError_t copy_cols(double *dst, int64_t ldd, const double *src, int64_t lds, int64_t rows, int64_t cols,
+                      cudaMemcpyKind kind, cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    if ((ldd == rows && lds == rows) || cols == 1)
+        return cudaMemcpyAsync(dst, src, 8 * (size_t)rows * (size_t)cols, kind, s);
+    return cudaMemcpy2DAsync(dst, 8 * (size_t)ldd, src, 8 * (size_t)lds, 8 * (size_t)rows, (size_t)cols, kind, s);
 }
 
 // ---- workspace ---------------------------------------------------------------
@@ -638,9 +584,26 @@ struct HostOut {
     cudaEvent_t ev = nullptr;
 };
 
+// Host-input pipeline (aqr_gs_factor_pinned): Z arrives in column chunks on
+// an H2D stream.  A chunk joins the live columns when the step loop needs
+// it, after a catch-up of the steps already done: the trailing passes
+// k = 0 .. i-1 over the chunk's columns (left-looking MGS on the chunk), with
+// the same (tile, column) units, deferred updates and reduction trees as the
+// main loop -- results are bitwise those of the device-resident call.  The
+// step vectors (HA: x_k, HP / naive: p_k) are kept for all k (vall).
+struct Pipe {
+    std::vector<int64_t> bounds;  // chunk c = columns [bounds[c], bounds[c + 1])
+    std::vector<cudaEvent_t> ev;  // H2D of chunk c complete
+    double *vall = nullptr;       // m x n
+    double *partial2 = nullptr;   // catch-up partials, n x ntiles
+    size_t next = 0;
+};
+
 struct Run {
     aqr_factor_args *a;
     HostOut *ho = nullptr;
+    Pipe *pp = nullptr;
+    int64_t live = 0;  // columns [0, live) are resident and caught up
     cudaStream_t s;
     bool hp, cgs, naive, csr_native;
     int64_t m, n;
@@ -651,6 +614,7 @@ struct Run {
     double *Rt, *partial, *npart, *xvec, *zvec, *pvec, *pring, *P, *X, *Z0;
     int64_t mv = 0;
     bool pending = false;  // row i-1 of R left as trailing partials (RrowIn)
+    int32_t pending_cols = 0;
 
     double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
 
@@ -659,8 +623,8 @@ struct Run {
         if (!ho || !ho->qhost) return AQR_OK;
         AQR_CUDA(cudaEventRecord(ho->ev, s));
         AQR_CUDA(cudaStreamWaitEvent(ho->cs, ho->ev, 0));
-        AQR_CUDA(cudaMemcpyAsync(ho->qhost + j * ho->ldqh, W + j * ldw, 8 * (size_t)m, cudaMemcpyDeviceToHost,
-                                 ho->cs));
+        AQR_CUDA(copy_cols(ho->qhost + j * ho->ldqh, ho->ldqh, W + j * ldw, ldw, m, 1, cudaMemcpyDeviceToHost,
+                           ho->cs));
         return AQR_OK;
     }
 
@@ -668,7 +632,7 @@ struct Run {
         aqr::RrowIn in;
         in.partial = partial;
         in.ntiles = (int32_t)aqr::num_tiles(m);
-        in.ncols = (int32_t)(n - j);
+        in.ncols = pending_cols;
         in.rrow = rt(j - 1, j);
         return in;
     }
@@ -692,6 +656,39 @@ struct Run {
         return o;
     }
 
+    // Where step j's vector goes: HA x_j (xout), HP / naive p_j (pout_slot).
+    double *xout(int64_t j) const { return (pp && !hp && !naive) ? pp->vall + j * m : xvec; }
+    double *pout_slot(int64_t j) const {
+        if (pp) return pp->vall + j * m;
+        return hp ? pring + (j & 1) * m : pvec;
+    }
+
+    // Bring the next chunk of Z in at step i (Pipe): wait for its H2D, form
+    // its X = A Z (HP) / saved copy (CGS), then run steps 0 .. i-1's trailing
+    // passes over it (totals by rrow_reduce into R).
+    aqr_status make_live(int64_t i) {
+        const size_t c = pp->next++;
+        const int64_t c0 = pp->bounds[c], c1 = pp->bounds[c + 1], w = c1 - c0;
+        AQR_CUDA(cudaStreamWaitEvent(s, pp->ev[c], 0));
+        if (cgs)
+            AQR_CUDA(copy_cols(col(Z0, m, c0), m, col(W, ldw, c0), ldw, m, w, cudaMemcpyDeviceToDevice, s));
+        if (hp) {  // X = op.apply_block(Zw), chunk by chunk
+            AQR_TRY(op_apply(a->op, w, col(W, ldw, c0), ldw, col(X, m, c0), m, s));
+            mv += w;
+        }
+        for (int64_t k = 0; k < i; ++k) {
+            aqr::TrailArgs t = trail(k, c0, c1);
+            t.qprev = k > 0 ? col(W, ldw, k - 1) : nullptr;
+            t.pprev = (hp && k > 0) ? pp->vall + (k - 1) * m : nullptr;
+            t.psrc = pp->vall + k * m;
+            t.rii = (hp || naive) ? nullptr : rt(k, k);
+            t.partial = pp->partial2;
+            AQR_TRY(launch_trailing(t, hp, cgs, s));
+        }
+        live = c1;
+        return AQR_OK;
+    }
+
     // Column j receives the deferred projection r_{j-1,j} (z_j and, for HP,
     // x_j); x = A z (HA/naive); then t = z.x, |z|, |x| -> R[j,j] and the
     // breakdown / flag record (normalize(j), gram_schmidt.py:148-160).
@@ -712,22 +709,24 @@ struct Run {
         } else if (csr_native) {
             // one fused launch: r_{j-1,j} (and the rest of row j-1 of R),
             // gather (z - r q), x = A z, z_new, norm, r_jj
-            AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s, pin));
+            double *xo = xout(j);
+            AQR_TRY(launch_csr(a->op, 1, z, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
             static const int rep = [] {  // diagnostics: idempotent repeats of the step
                 const char *e = std::getenv("AQR_SPMV_REPEAT");
                 return e ? std::atoi(e) : 0;
             }();
             for (int k = 0; k < rep; ++k)
-                AQR_TRY(launch_csr(a->op, 1, z, m, xvec, m, qprev, r, zvec, norm_out(j), s, pin));
+                AQR_TRY(launch_csr(a->op, 1, z, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
             ++mv;
             zcol = zvec;
-            xcol = xvec;
+            xcol = xo;
         } else {
+            double *xo = xout(j);
             if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, no_norm(), s));
-            AQR_TRY(mv1(z, xvec));  // op.apply(Zw[:, j].copy()), line 151
-            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xvec, norm_out(j), s));
+            AQR_TRY(mv1(z, xo));  // op.apply(Zw[:, j].copy()), line 151
+            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xo, norm_out(j), s));
             zcol = z;
-            xcol = xvec;
+            xcol = xo;
         }
         return AQR_OK;
     }
@@ -754,33 +753,36 @@ struct Run {
     }
 
     aqr_status row_form() {
+        live = pp ? 0 : n;
         for (int64_t i = 0; i < n; ++i) {
             const auto hs = std::chrono::steady_clock::now();
-            const double *pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
+            while (live <= i) AQR_TRY(make_live(i));
+            const double *pprev = (hp && i > 0) ? pout_slot(i - 1) : nullptr;
             const double *zcol = nullptr, *xcol = nullptr;
             AQR_TRY(norm_step(i, pprev, zcol, xcol));
-            aqr::TrailArgs t = trail(i, i + 1, n);
+            aqr::TrailArgs t = trail(i, i + 1, std::max<int64_t>(i + 1, live));
             t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
             t.pprev = pprev;
             t.reverse = (int32_t)(i & 1);
             if (naive) {
                 // q_i first, then p_i = A q_i (lines 161-163)
                 AQR_TRY(launch_normalize(m, zcol, rt(i, i), col(W, ldw, i), nullptr, nullptr, status, s));
-                AQR_TRY(mv1(col(W, ldw, i), pvec));
-                t.psrc = pvec;
+                AQR_TRY(mv1(col(W, ldw, i), pout_slot(i)));
+                t.psrc = pout_slot(i);
                 t.rii = nullptr;
             } else {
                 t.psrc = xcol;
                 t.rii = rt(i, i);
                 t.zsrc = zcol;
                 t.qout = col(W, ldw, i);
-                t.pout = hp ? pring + (i & 1) * m : nullptr;
+                t.pout = hp ? pout_slot(i) : nullptr;
             }
             {
                 static const bool dbg = std::getenv("AQR_DEBUG_TIMING") != nullptr;
                 const auto h0 = std::chrono::steady_clock::now();
                 const bool can_defer = (hp || csr_native) && i + 1 < n && defer_mode() != 0;
                 AQR_TRY(launch_trailing(t, hp, cgs, s, can_defer ? &pending : nullptr));
+                pending_cols = t.jend - t.jbeg;
                 AQR_TRY(col_final(i));
                 if (dbg) {
                     const auto h1 = std::chrono::steady_clock::now();
@@ -789,74 +791,6 @@ struct Run {
                                  std::chrono::duration<double, std::micro>(h0 - hs).count());
                 }
             }
-        }
-        return AQR_OK;
-    }
-
-    // Norm step of column j on stream st (look-ahead schedule): HP updates
-    // z_j, x_j and forms the norm; native CSR HA runs the fused SpMV step
-    // into ring slot j & 1.
-    aqr_status norm_step_la(int64_t j, cudaStream_t st, const double *&zcol, const double *&xcol) {
-        double *z = col(W, ldw, j);
-        const double *qprev = j > 0 ? col(W, ldw, j - 1) : nullptr;
-        const double *r = j > 0 ? rt(j - 1, j) : nullptr;
-        if (hp) {
-            const double *pprev = j > 0 ? pring + ((j - 1) & 1) * m : nullptr;
-            double *x = col(X, m, j);
-            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev, r, nullptr, norm_out(j), st));
-            zcol = z;
-            xcol = x;
-        } else {
-            double *xs = xvec + (j & 1) * m, *zs = zvec + (j & 1) * m;
-            AQR_TRY(launch_csr(a->op, 1, z, m, xs, m, qprev, r, zs, norm_out(j), st));
-            ++mv;
-            zcol = zs;
-            xcol = xs;
-        }
-        return AQR_OK;
-    }
-
-    // Look-ahead row form (native CSR HA, HP).  Step i's trailing pass is
-    // split: T_first updates column i+1 and forms r_{i,i+1} (and stores
-    // q_i, p_i); then the norm step of column i+1 (the latency-bound SpMV
-    // for HA) runs on the side stream concurrently with T_rest, the
-    // bandwidth-bound pass over columns i+2..n-1.  Same kernels, same
-    // per-element operations and reduction trees: bitwise identical to
-    // row_form().
-    aqr_status row_form_lookahead(cudaStream_t side, cudaEvent_t e1, cudaEvent_t e2) {
-        const double *zc = nullptr, *xc = nullptr;
-        AQR_TRY(norm_step_la(0, s, zc, xc));
-        for (int64_t i = 0; i < n; ++i) {
-            const double *pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
-            aqr::TrailArgs t = trail(i, i + 1, std::min<int64_t>(i + 2, n));
-            t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
-            t.pprev = pprev;
-            t.reverse = (int32_t)(i & 1);
-            t.psrc = xc;
-            t.rii = rt(i, i);
-            t.zsrc = zc;
-            t.qout = col(W, ldw, i);
-            t.pout = hp ? pring + (i & 1) * m : nullptr;
-            AQR_TRY(launch_trailing(t, hp, cgs, s));  // T_first (vector-only at i = n-1)
-            AQR_TRY(col_final(i));
-            if (i + 1 >= n) break;
-            AQR_CUDA(cudaEventRecord(e1, s));
-            AQR_CUDA(cudaStreamWaitEvent(side, e1, 0));
-            const double *zn = nullptr, *xn = nullptr;
-            AQR_TRY(norm_step_la(i + 1, side, zn, xn));
-            AQR_CUDA(cudaEventRecord(e2, side));
-            if (i + 2 < n) {  // T_rest: columns i+2.., q_i / p_i already stored
-                aqr::TrailArgs t2 = trail(i, i + 2, n);
-                t2.qprev = t.qprev;
-                t2.pprev = pprev;
-                t2.reverse = t.reverse;
-                t2.psrc = xc;
-                t2.rii = rt(i, i);
-                AQR_TRY(launch_trailing(t2, hp, cgs, s));
-            }
-            AQR_CUDA(cudaStreamWaitEvent(s, e2, 0));
-            zc = zn;
-            xc = xn;
         }
         return AQR_OK;
     }
@@ -963,7 +897,7 @@ aqr_status aqr_status_init(int32_t *status, int64_t n, void *stream) {
     return launched("status_init_kernel");
 }
 
-static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho) {
+static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, Pipe *pp = nullptr) {
     if (!a) return set_err(AQR_EARG, "null args");
     a->fail_col = -1;
     a->fail_val = 0.0;
@@ -984,6 +918,7 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho) 
     Run r;
     r.a = a;
     r.ho = ho;
+    r.pp = (pp && a->orientation == AQR_ROW) ? pp : nullptr;
     r.s = S(stream);
     r.hp = a->variant == AQR_HP;
     r.naive = a->variant == AQR_NAIVE;
@@ -1009,34 +944,21 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho) 
     cudaStream_t s = r.s;
 
     if (a->Z != a->Q)  // Zw = Z.copy(order="F"), line 131
-        AQR_CUDA(cudaMemcpy2DAsync(a->Q, a->ldq * 8, a->Z, a->ldz * 8, m * 8, n, cudaMemcpyDeviceToDevice, s));
+        AQR_CUDA(copy_cols(a->Q, a->ldq, a->Z, a->ldz, m, n, cudaMemcpyDeviceToDevice, s));
     AQR_TRY(aqr_status_init(r.status, n, stream));
     AQR_CUDA(cudaMemsetAsync(r.counters, 0, 4 * (size_t)(n + 8), s));
     AQR_CUDA(cudaMemsetAsync(r.Rt, 0, 8 * (size_t)n * n, s));
-    if (r.cgs)  // Z0, line 132
-        AQR_CUDA(cudaMemcpy2DAsync(r.Z0, m * 8, a->Q, a->ldq * 8, m * 8, n, cudaMemcpyDeviceToDevice, s));
-    if (r.hp) {  // X = op.apply_block(Zw)
+    if (r.cgs && !r.pp)  // Z0, line 132 (per chunk when pipelined)
+        AQR_CUDA(copy_cols(r.Z0, m, a->Q, a->ldq, m, n, cudaMemcpyDeviceToDevice, s));
+    if (r.hp && !r.pp) {  // X = op.apply_block(Zw), line 136 (per chunk when pipelined)
         AQR_TRY(op_apply(a->op, n, a->Q, a->ldq, r.X, m, s));
         r.mv += n;
     }
     static const bool debug_timing = std::getenv("AQR_DEBUG_TIMING") != nullptr;
     const auto t_loop = std::chrono::steady_clock::now();
-    L2Window l2w;
-    AQR_TRY(l2_window_begin(a->op, s, l2w));
-    const bool lookahead = a->orientation == AQR_ROW && lookahead_mode() != 0 &&
-                           (r.hp || (r.csr_native && a->variant == AQR_HA));
-    if (lookahead) {
-        SideCtx sc;
-        AQR_TRY(side_acquire(sc));
-        const aqr_status st_la = r.row_form_lookahead(sc.side, sc.e1, sc.e2);
-        side_release(sc);
-        AQR_TRY(st_la);
-    } else {
-        AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
-    }
+    AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
     aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, r.Rt, a->R, a->ldr);
     AQR_TRY(launched("finalize_r_kernel"));
-    l2_window_end(l2w);
     std::vector<int32_t> st((16 + 4 * n) / 4);
     AQR_CUDA(cudaMemcpyAsync(st.data(), r.status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
     const auto t_enq = std::chrono::steady_clock::now();
@@ -1058,6 +980,93 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho) 
 }
 
 aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) { return gs_factor_impl(a, stream, nullptr); }
+
+// The pipeline's extra buffers come from the device's default stream-ordered
+// pool; keep freed blocks in the pool (release threshold = max) so repeated
+// calls do not map and unmap hundreds of MB each time.
+static void keep_pool_memory() {
+    static std::mutex mu;
+    static std::vector<int> done;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int d : done)
+        if (d == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done.push_back(dev);
+}
+
+aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_t ldzh, double *Q_host,
+                                int64_t ldqh, double *R_host, int64_t ldrh, int64_t chunk_cols, void *stream) {
+    if (!a || !Z_host || !Q_host || !R_host) return set_err(AQR_EARG, "null args / host buffers");
+    const int64_t m = a->m, n = a->n;
+    if (n < 1 || m < n) return set_err(AQR_EDIM, "need m >= n >= 1");
+    if (!a->Q || ldzh < m || ldqh < m || ldrh < n || a->ldq < m) return set_err(AQR_EARG, "bad buffers / leading dimensions");
+    cudaStream_t s = S(stream);
+    a->Z = a->Q;  // Z is staged into Q (factorized in place)
+    a->ldz = a->ldq;
+    if (a->orientation != AQR_ROW) {  // column form: whole H2D first, then the streamed D2H
+        AQR_CUDA(copy_cols(a->Q, a->ldq, Z_host, ldzh, m, n, cudaMemcpyHostToDevice, s));
+        return aqr_gs_factor_d2h(a, Q_host, ldqh, R_host, ldrh, stream);
+    }
+    const int64_t w = chunk_cols > 0 ? chunk_cols : std::max<int64_t>(1, (n + 7) / 8);
+    Pipe pp;
+    for (int64_t c0 = 0; c0 < n; c0 += w) pp.bounds.push_back(c0);
+    pp.bounds.push_back(n);
+    const size_t nch = pp.bounds.size() - 1;
+    const int64_t ntiles = std::max<int64_t>(aqr::num_tiles(m), 1);
+    keep_pool_memory();
+    AQR_CUDA(cudaMallocAsync((void **)&pp.vall, 8 * (size_t)m * n, s));
+    AQR_CUDA(cudaMallocAsync((void **)&pp.partial2, 8 * (size_t)n * ntiles, s));
+    SideCtx h2d;
+    AQR_TRY(side_acquire(h2d));
+    aqr_status st = AQR_OK;
+    // the H2D stream starts after everything already queued on `stream`
+    if (cudaEventRecord(h2d.e1, s) != cudaSuccess || cudaStreamWaitEvent(h2d.side, h2d.e1, 0) != cudaSuccess)
+        st = set_err(AQR_ECUDA, "h2d stream ordering");
+    for (size_t c = 0; c < nch && st == AQR_OK; ++c) {
+        cudaEvent_t e = nullptr;
+        const int64_t c0 = pp.bounds[c], cw = pp.bounds[c + 1] - c0;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+            st = set_err(AQR_ECUDA, "event");
+            break;
+        }
+        pp.ev.push_back(e);
+        if (copy_cols(a->Q + c0 * a->ldq, a->ldq, Z_host + c0 * ldzh, ldzh, m, cw, cudaMemcpyHostToDevice,
+                      h2d.side) != cudaSuccess ||
+            cudaEventRecord(e, h2d.side) != cudaSuccess)
+            st = set_err(AQR_ECUDA, "H2D Z chunk");
+    }
+    if (st == AQR_OK) {
+        SideCtx d2h;
+        st = side_acquire(d2h);
+        if (st == AQR_OK) {
+            HostOut ho;
+            ho.qhost = Q_host;
+            ho.ldqh = ldqh;
+            ho.cs = d2h.side;
+            ho.ev = d2h.e1;
+            st = gs_factor_impl(a, stream, &ho, &pp);
+            if (st == AQR_OK &&
+                cudaMemcpy2DAsync(R_host, 8 * (size_t)ldrh, a->R, 8 * (size_t)a->ldr, 8 * (size_t)n, (size_t)n,
+                                  cudaMemcpyDeviceToHost, s) != cudaSuccess)
+                st = set_err(AQR_ECUDA, "D2H R");
+            if (cudaStreamSynchronize(d2h.side) != cudaSuccess && st == AQR_OK) st = set_err(AQR_ECUDA, "D2H Q");
+            side_release(d2h);
+        }
+    }
+    cudaStreamSynchronize(h2d.side);
+    side_release(h2d);
+    for (cudaEvent_t e : pp.ev) cudaEventDestroy(e);
+    cudaFreeAsync(pp.vall, s);
+    cudaFreeAsync(pp.partial2, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && st == AQR_OK) st = set_err(AQR_ECUDA, "stream");
+    return st;
+}
 
 aqr_status aqr_gs_factor_d2h(aqr_factor_args *a, double *Q_host, int64_t ldqh, double *R_host, int64_t ldrh,
                              void *stream) {

@@ -173,6 +173,12 @@ def _expected_mv(variant, n, fail_col):
     return 2 * fail_col + 1 if variant == "naive" else fail_col + 1
 
 
+def _chunk_cols():
+    import os
+
+    return int(os.environ.get("AQR_CHUNK_COLS", "0"))  # 0: the library's default (n / 8)
+
+
 def _gs_factor(Z, op, family, variant, orientation):
     """The factorization driver (gram_schmidt.py:126-179) on the device."""
     Z, m, n = _check_inputs(Z, op)
@@ -181,8 +187,14 @@ def _gs_factor(Z, op, family, variant, orientation):
     back = _result_converter(Z)
     mv_before = op.mv_count
 
-    Zd, ldz = D.to_device_f(Z)
-    Q = D.empty_f(m, n)
+    host_in = not (D.is_torch(Z) and Z.is_cuda)
+    if host_in:  # Z stays on the host; aqr_gs_factor_pinned streams it in
+        Zh, ldzh = D.to_pinned_f(Z)
+        Q = D.empty_f(m, n)
+        Zd, ldz = Q, m
+    else:
+        Zd, ldz = D.to_device_f(Z)
+        Q = D.empty_f(m, n)
     R = D.empty_f(n, n)
     fam, var, ori = _lib.FAMILY_CODE[family], _lib.VARIANT_CODE[variant], _lib.ORIENTATION_CODE[orientation]
     ws = t.empty(int(L.aqr_workspace_bytes(fam, var, ori, m, n)), dtype=t.uint8, device=Q.device)
@@ -201,14 +213,16 @@ def _gs_factor(Z, op, family, variant, orientation):
     a.op = ctypes.pointer(desc)
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     a.flagged_host = flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
-    if not (D.is_torch(Z) and Z.is_cuda):
-        # host input (numpy or CPU tensor): Q columns stream back into
-        # page-locked host memory while the later steps run
-        # (aqr_gs_factor_d2h); numpy callers get F-ordered views of it (the
-        # page-locked block returns to torch's host cache when they drop it)
+    if host_in:
+        # host input (numpy or CPU tensor): Z streams in by column chunks and
+        # Q columns stream back into page-locked host memory, both overlapped
+        # with the steps (aqr_gs_factor_pinned); numpy callers get F-ordered
+        # views of the page-locked block (it returns to torch's host cache
+        # when they drop it)
         Qh = t.empty((n, m), dtype=t.float64, pin_memory=True).t()
         Rh = t.empty((n, n), dtype=t.float64, pin_memory=True).t()
-        status = L.aqr_gs_factor_d2h(ctypes.byref(a), Qh.data_ptr(), m, Rh.data_ptr(), n, D.stream_ptr())
+        status = L.aqr_gs_factor_pinned(ctypes.byref(a), Zh.data_ptr(), ldzh, Qh.data_ptr(), m, Rh.data_ptr(), n,
+                                        _chunk_cols(), D.stream_ptr())
         if D.is_torch(Z):
             back = lambda T: Qh if T is Q else Rh  # noqa: E731
         else:
@@ -229,6 +243,8 @@ def _gs_factor(Z, op, family, variant, orientation):
         raise DimensionError(L.aqr_last_error().decode())
     _lib.check(status, "aqr_gs_factor")
     del Zd, ws
+    if host_in:
+        del Zh
     cost = CostReport(op.mv_count - mv_before, _model_flops(family, variant, m, n))
     return QrResult(back(Q), back(R), cost, [int(j) for j in np.flatnonzero(flags)])
 

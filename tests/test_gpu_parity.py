@@ -266,11 +266,16 @@ def test_operator_counts_and_errors(aqr):
         op.apply_block(np.ones((2, 2)))
 
 
-@pytest.mark.parametrize("meth", ["mgs-ha-row", "mgs-hp-row", "mgs-naive-col"])
-def test_pinned_host_input_streams_q_bitwise(aqr, meth):
-    """Page-locked host Z: Q columns stream back while later steps run
-    (aqr_gs_factor_d2h); results equal the device-resident call bitwise."""
+@pytest.mark.parametrize("meth,chunk", [("mgs-ha-row", 0), ("mgs-ha-row", 1), ("mgs-ha-row", 3),
+                                        ("mgs-hp-row", 0), ("mgs-hp-row", 4), ("mgs-naive-row", 3),
+                                        ("cgs-ha-row", 3), ("cgs-hp-row", 0), ("mgs-naive-col", 0)])
+def test_pinned_host_input_streams_q_bitwise(aqr, meth, chunk, monkeypatch):
+    """Page-locked host Z: Z streams in by column chunks (each chunk replays
+    the steps already done) and Q streams back while later steps run
+    (aqr_gs_factor_pinned); results equal the device-resident call bitwise."""
     import torch
+
+    monkeypatch.setenv("AQR_CHUNK_COLS", str(chunk))
 
     from paper_1703_10440_b200 import problems
 
