@@ -1134,7 +1134,12 @@ aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientati
     } else if (st == AQR_OK && op_kind == AQR_OP_CSR) {
         ip32.resize(m + 1);
         ix32.resize(nnz);
-        for (int64_t i = 0; i <= m; ++i) ip32[i] = (int32_t)indptr_host[i];
+        int64_t longest = 0;
+        for (int64_t i = 0; i <= m; ++i) {
+            ip32[i] = (int32_t)indptr_host[i];
+            if (i > 0) longest = std::max<int64_t>(longest, indptr_host[i] - indptr_host[i - 1]);
+        }
+        op.max_row_nnz = (int32_t)std::min<int64_t>(longest, INT32_MAX);
         for (int64_t k = 0; k < nnz; ++k) ix32[k] = (int32_t)indices_host[k];
         int32_t *ip = (int32_t *)dalloc(4 * (size_t)(m + 1));
         int32_t *ix = (int32_t *)dalloc(4 * (size_t)nnz);
