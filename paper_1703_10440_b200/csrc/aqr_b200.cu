@@ -241,18 +241,18 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
             return e ? std::atoi(e) : 0;
         }();
         const unsigned g1 = (unsigned)nt;  // the canonical norm grid
-        ensure_carveout(aqr::csr_step_kernel<8, 4>);
+        ensure_carveout(aqr::csr_step_kernel<8, aqr::kNormMinBlocks>);
         // row batch B = the longest row when known and <= 8 (all of a row's
         // loads in one batch, no predicated-off slots); longer rows loop
         const int32_t mr = op->max_row_nnz;
         if (sv == 0 && mr >= 1 && mr <= 4)
-            launch_pdl(aqr::csr_step_kernel<4, 4>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_kernel<4, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
         else if (sv == 0 && mr == 5)
-            launch_pdl(aqr::csr_step_kernel<5, 4>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_kernel<5, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
         else if (sv == 0 && mr == 6)
-            launch_pdl(aqr::csr_step_kernel<6, 4>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_kernel<6, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
         else if (sv == 0 || sv == 3)
-            launch_pdl(aqr::csr_step_kernel<8, 4>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_kernel<8, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
         else
             launch_pdl(aqr::csr_step_kernel<8, 1>, g1, aqr::kBlock, 0, s, a);
         timer_end(tix, s);

@@ -56,6 +56,11 @@ __host__ __device__ inline int64_t num_tiles(int64_t m) {
 #define AQR_NORM_GRID (148 * 4)
 #endif
 constexpr int kNormGrid = AQR_NORM_GRID;
+// CTAs per SM the norm-grid kernels are compiled for (the grid is one wave).
+#ifndef AQR_NORM_MINB
+#define AQR_NORM_MINB 4
+#endif
+constexpr int kNormMinBlocks = AQR_NORM_MINB;
 __host__ __device__ inline int64_t norm_tiles(int64_t m) {
     const int64_t b = (m + kBlock - 1) / kBlock;
     return b < kNormGrid ? b : kNormGrid;
@@ -337,7 +342,7 @@ struct ColArgs {
 // processed per iteration with all their loads in flight, rows accumulated
 // in ascending block order.
 constexpr int kColTiles = 4;
-__global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
+__global__ void __launch_bounds__(kBlock, kNormMinBlocks) col_update_norm_kernel(ColArgs a) {
     pdl_wait();
     if (failed(a.out.status)) return;
     const bool upd = a.r != nullptr;
