@@ -196,13 +196,16 @@ AQR_API int64_t aqr_num_tiles(int64_t m);
 
 /* z_i -= r * q_{i-1} (and x_i -= r * p_{i-1} when x/pprev given) where
  * r = r_dev[0] (skipped when r_dev == NULL); then, if npart != NULL, the
- * per-tile partials of (z.x, z.z, x.x) into npart[3 * ntiles]. */
+ * per-CTA partials of (z.x, z.z, x.x) into npart (3 x the variant's norm
+ * grid; HP when x is given, HA / naive otherwise). */
 AQR_API aqr_status aqr_step_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
                                     const double *pprev, const double *r_dev,
                                     const double *xnorm, double *npart, const int32_t *status,
                                     void *stream);
-/* tot[0..2] = fixed-order sums of npart (for the all-reduce) */
-AQR_API aqr_status aqr_step_norm_reduce(int64_t m, const double *npart, double *tot,
+/* tot[0..2] = fixed-order sums of npart (for the all-reduce).  `variant`
+ * (aqr_variant) selects the norm grid the partials were formed on: HP
+ * (aqr_step_col_update_norm called with x) or HA / naive (called with xnorm). */
+AQR_API aqr_status aqr_step_norm_reduce(int64_t m, int32_t variant, const double *npart, double *tot,
                                 const int32_t *status, void *stream);
 /* From tot: breakdown check (status), flag, R[i,i] = sqrt(t) into rii. */
 AQR_API aqr_status aqr_step_norm_finish(int64_t i, const double *tot, double *rii, int32_t *status,
@@ -250,6 +253,11 @@ AQR_API aqr_status aqr_kernel_timer_read(int32_t slot, int64_t *launches, double
 /* Per-launch device times (ms) and algorithmic bytes of a slot, in launch
  * order; returns the number of timed launches (-1 on a CUDA error). */
 AQR_API int64_t aqr_kernel_timer_list(int32_t slot, double *ms_out, double *bytes_out, int64_t max);
+/* Diagnostics: per-launch trace of the fused SpMV step and trailing kernels
+ * (3 x uint64 per launch: first-CTA start before / after the dependency wait,
+ * last-CTA end, %globaltimer ns) in libraries built with -DAQR_TRACE; returns
+ * the number of launches recorded, or -1 in production builds. */
+AQR_API int64_t aqr_trace_read(uint64_t *out, int64_t max_slots);
 
 AQR_API const char *aqr_last_error(void);
 AQR_API int32_t aqr_abi_version(void);

@@ -61,6 +61,7 @@ class AqrFactorArgs(ctypes.Structure):
 SIGNATURES = {
     "aqr_workspace_bytes": (c_u64, [c_i32, c_i32, c_i32, c_i64, c_i64]),
     "aqr_gs_factor": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp]),
+    "aqr_trace_read": (c_i64, [c_vp, c_i64]),
     "aqr_gs_factor_d2h": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_gs_factor_pinned": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                      c_i64, c_vp]),
@@ -77,7 +78,7 @@ SIGNATURES = {
     "aqr_tile_rows": (c_i64, [c_i64]),
     "aqr_num_tiles": (c_i64, [c_i64]),
     "aqr_step_col_update_norm": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "aqr_step_norm_reduce": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "aqr_step_norm_reduce": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "aqr_step_norm_finish": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "aqr_step_normalize": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "aqr_step_trailing": (c_i32, [c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,

@@ -201,6 +201,27 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
     cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// ---- diagnostics: kernel trace (AQR_TRACE builds) ----------------------------
+#ifdef AQR_TRACE
+struct Trace {
+    unsigned long long *dev = nullptr;
+    int32_t next = 0, cap = 0;
+} g_tr;
+int32_t trace_slot() {
+    if (!g_tr.dev) {
+        g_tr.cap = 1 << 14;
+        cudaMalloc(&g_tr.dev, 3 * sizeof(unsigned long long) * g_tr.cap);
+        cudaMemcpyToSymbol(aqr::g_trace, &g_tr.dev, sizeof(g_tr.dev));
+        std::vector<unsigned long long> init(3 * g_tr.cap);
+        for (int i = 0; i < g_tr.cap; ++i) init[3 * i] = init[3 * i + 1] = ~0ull, init[3 * i + 2] = 0;
+        cudaMemcpy(g_tr.dev, init.data(), init.size() * 8, cudaMemcpyHostToDevice);
+    }
+    return g_tr.next < g_tr.cap ? g_tr.next++ : -1;
+}
+#else
+int32_t trace_slot() { return -1; }
+#endif
+
 // ---- operators ---------------------------------------------------------------
 
 aqr::NormOut no_norm() {
@@ -214,6 +235,7 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
                       const aqr::NormOut &out, cudaStream_t s, const aqr::RrowIn *rin = nullptr) {
     aqr::CsrArgs a;
     std::memset(&a.rin, 0, sizeof a.rin);
+    a.trace = out.npart != nullptr ? trace_slot() : -1;
     if (rin && out.npart != nullptr) a.rin = *rin;
     a.m = op->m;
     a.k = k;
@@ -234,27 +256,31 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
     const int64_t nblocks = (op->m + aqr::kBlock - 1) / aqr::kBlock;
     const int64_t grid = std::min<int64_t>(nblocks, (int64_t)sm_count() * 8);
     if (out.npart != nullptr) {
-        const int64_t nt = aqr::norm_tiles(op->m);
+        const int64_t nt = aqr::norm_tiles(op->m, false);
         const long tix = timer_begin(1, (double)op->m * 40.0 + (double)op->nnz * 12.0, s);
         static const int sv = [] {
             const char *e = std::getenv("AQR_SPMV_VARIANT");
             return e ? std::atoi(e) : 0;
         }();
-        const unsigned g1 = (unsigned)nt;  // the canonical norm grid
-        ensure_carveout(aqr::csr_step_kernel<8, aqr::kNormMinBlocks>);
-        // row batch B = the longest row when known and <= 8 (all of a row's
-        // loads in one batch, no predicated-off slots); longer rows loop
+        const unsigned g1 = (unsigned)nt;  // the canonical norm grid (HA / naive)
+        // software-pipelined fused step; row batch B = the longest row when
+        // known and <= 8 (all of a row's loads in one batch, no predicated-off
+        // slots); longer rows loop.  AQR_SPMV_VARIANT=3: unpipelined, B = 8.
         const int32_t mr = op->max_row_nnz;
-        if (sv == 0 && mr >= 1 && mr <= 4)
-            launch_pdl(aqr::csr_step_kernel<4, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
-        else if (sv == 0 && mr == 5)
-            launch_pdl(aqr::csr_step_kernel<5, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
-        else if (sv == 0 && mr == 6)
-            launch_pdl(aqr::csr_step_kernel<6, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
-        else if (sv == 0 || sv == 3)
-            launch_pdl(aqr::csr_step_kernel<8, aqr::kNormMinBlocks>, g1, aqr::kBlock, 0, s, a);
-        else
-            launch_pdl(aqr::csr_step_kernel<8, 1>, g1, aqr::kBlock, 0, s, a);
+        if (sv == 3)
+            launch_pdl(aqr::csr_step_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
+        else if (mr >= 1 && mr <= 4)
+            launch_pdl(aqr::csr_step_pf_kernel<4, 3>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 5)
+            launch_pdl(aqr::csr_step_pf_kernel<5, 3>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 6)
+            launch_pdl(aqr::csr_step_pf_kernel<6, 3>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 7)
+            launch_pdl(aqr::csr_step_pf_kernel<7, 3>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 8)
+            launch_pdl(aqr::csr_step_pf_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
+        else  // long or unknown rows: batches of 8 without the row look-ahead
+            launch_pdl(aqr::csr_step_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
         timer_end(tix, s);
         return launched("csr_step_kernel");
     }
@@ -327,10 +353,11 @@ aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, d
 
 aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
                                   const double *pprev, const double *r, const double *xnorm,
-                                  const aqr::NormOut &out, cudaStream_t s,
+                                  const aqr::NormOut &out, bool hp_grid, cudaStream_t s,
                                   const aqr::RrowIn *rin = nullptr) {
     aqr::ColArgs a;
     std::memset(&a.rin, 0, sizeof a.rin);
+    a.trace = out.npart != nullptr ? trace_slot() : -1;
     if (rin) a.rin = *rin;
     a.m = m;
     a.z = z;
@@ -340,8 +367,8 @@ aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, dou
     a.r = r;
     a.xnorm = xnorm;
     a.out = out;
-    a.out.ntiles = (int32_t)aqr::norm_tiles(m);
-    const int64_t nt = aqr::norm_tiles(m);
+    a.out.ntiles = (int32_t)aqr::norm_tiles(m, hp_grid);
+    const int64_t nt = aqr::norm_tiles(m, hp_grid);
     if (nt == 0) return AQR_OK;
     const int64_t grid = nt;  // the canonical norm grid (also without norm output)
     ensure_carveout(aqr::col_update_norm_kernel);
@@ -384,7 +411,9 @@ aqr_status launch_rrow_reduce(int64_t m, int64_t ncols, const double *partial, d
 aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStream_t s,
                            bool *deferred = nullptr) {
     if (deferred) *deferred = false;
+    const int32_t tslot = trace_slot();
     aqr::TrailArgs a = a0;
+    a.trace = tslot;
     const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
     if (a.ntiles == 0) return AQR_OK;
     const bool big = aqr::rows_per_thread(a.m) == 8;
@@ -554,7 +583,7 @@ Layout layout(int32_t family, int32_t variant, int32_t orientation, int64_t m, i
     L.counters = take(4 * (nn + 8));
     L.rt = take(8 * nn * nn);
     L.partial = take(8 * nn * ntiles);
-    L.npart = take(8 * 3 * std::max<uint64_t>((uint64_t)aqr::norm_tiles(m), 1));
+    L.npart = take(8 * 3 * std::max<uint64_t>((uint64_t)aqr::norm_tiles(m, variant == AQR_HP), 1));
     L.xvec = variant != AQR_HP ? take(8 * 2 * mm) : kNone;  // 2-slot ring (look-ahead)
     L.zvec = variant != AQR_HP ? take(8 * 2 * mm) : kNone;
     L.pvec = (variant == AQR_NAIVE && orientation == AQR_ROW) ? take(8 * mm) : kNone;
@@ -647,7 +676,7 @@ struct Run {
     aqr::NormOut norm_out(int64_t j) const {
         aqr::NormOut o;
         o.npart = npart;
-        o.ntiles = (int32_t)aqr::norm_tiles(m);
+        o.ntiles = (int32_t)aqr::norm_tiles(m, hp);
         o.counter = counters;
         o.tot = nullptr;
         o.rii = rt(j, j);
@@ -703,7 +732,7 @@ struct Run {
         pending = false;
         if (hp) {
             double *x = col(X, m, j);
-            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), s, pin));
+            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), true, s, pin));
             zcol = z;
             xcol = x;
         } else if (csr_native) {
@@ -722,9 +751,9 @@ struct Run {
             xcol = xo;
         } else {
             double *xo = xout(j);
-            if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, no_norm(), s));
+            if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, no_norm(), false, s));
             AQR_TRY(mv1(z, xo));  // op.apply(Zw[:, j].copy()), line 151
-            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xo, norm_out(j), s));
+            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xo, norm_out(j), false, s));
             zcol = z;
             xcol = xo;
         }
@@ -882,6 +911,22 @@ aqr_status aqr_trailing_timer_read(int64_t *launches, double *ms, double *bytes)
 }
 
 int32_t aqr_abi_version(void) { return AQR_ABI_VERSION; }
+
+// Diagnostics: copies the kernel trace (3 x uint64 per launch slot: first
+// CTA start before / after the dependency wait, last CTA end; globaltimer ns)
+// and returns the number of slots used; -1 when built without AQR_TRACE.
+int64_t aqr_trace_read(uint64_t *out, int64_t max_slots) {
+#ifdef AQR_TRACE
+    const int64_t n = std::min<int64_t>(g_tr.next, max_slots);
+    cudaDeviceSynchronize();
+    if (n > 0 && g_tr.dev) cudaMemcpy(out, g_tr.dev, 3 * 8 * (size_t)n, cudaMemcpyDeviceToHost);
+    return n;
+#else
+    (void)out;
+    (void)max_slots;
+    return -1;
+#endif
+}
 int64_t aqr_tile_rows(int64_t m) { return aqr::tile_rows(m); }
 int64_t aqr_num_tiles(int64_t m) { return aqr::num_tiles(m); }
 uint64_t aqr_status_bytes(int64_t n) { return 16 + 4 * (uint64_t)std::max<int64_t>(n, 0); }
@@ -1254,12 +1299,14 @@ aqr_status aqr_step_col_update_norm(int64_t m, double *z, const double *qprev, d
     aqr::NormOut o = no_norm();
     o.npart = npart;
     o.status = const_cast<int32_t *>(status);
-    return launch_col_update_norm(m, z, qprev, x, pprev, r_dev, xnorm, o, S(stream));
+    // HP carries x (passed as x); HA / naive pass the product as xnorm
+    return launch_col_update_norm(m, z, qprev, x, pprev, r_dev, xnorm, o, x != nullptr, S(stream));
 }
 
-aqr_status aqr_step_norm_reduce(int64_t m, const double *npart, double *tot, const int32_t *status,
-                                void *stream) {
-    aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, S(stream)>>>(npart, (int32_t)aqr::norm_tiles(m), tot, 0,
+aqr_status aqr_step_norm_reduce(int64_t m, int32_t variant, const double *npart, double *tot,
+                                const int32_t *status, void *stream) {
+    const bool hp = variant == AQR_HP;
+    aqr::norm_reduce_kernel<<<1, aqr::kBlock, 0, S(stream)>>>(npart, (int32_t)aqr::norm_tiles(m, hp), tot, 0,
                                                             nullptr, const_cast<int32_t *>(status));
     return launched("norm_reduce_kernel");
 }

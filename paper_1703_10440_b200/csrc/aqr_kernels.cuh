@@ -47,23 +47,26 @@ __host__ __device__ inline int64_t num_tiles(int64_t m) {
     return (m + t - 1) / t;
 }
 // The norm partials (z.x, z.z, x.x) are formed by a FIXED grid of
-// norm_tiles(m) = min(ceil(m/256), kNormGrid) CTAs: CTA b owns the 256-row
-// blocks b, b+G, b+2G, ...; thread k accumulates (fma) its row k of each owned
-// block in ascending block order; one block tree (warp xor butterfly, warps
-// ascending) per CTA gives partial b.  No barrier inside the row loop, one
-// per CTA at the end.  Totals are block_totals over the G partials.
-#ifndef AQR_NORM_GRID
-#define AQR_NORM_GRID (148 * 4)
+// norm_tiles(m, hp) = min(ceil(m/256), G) CTAs, G depending only on the
+// variant: CTA b owns the 256-row blocks b, b+G, b+2G, ...; thread k
+// accumulates (fma) its row k of each owned block in ascending block order;
+// one block tree (warp xor butterfly, warps ascending) per CTA gives partial
+// b.  Totals are block_totals over the G partials.  G is one wave of the
+// kernel that forms the partials: 3 CTAs/SM for the software-pipelined
+// fused SpMV step (HA / naive), 4 CTAs/SM for the HP column update.
+#ifndef AQR_NORM_GRID_HA
+#define AQR_NORM_GRID_HA (148 * 3)
 #endif
-constexpr int kNormGrid = AQR_NORM_GRID;
-// CTAs per SM the norm-grid kernels are compiled for (the grid is one wave).
-#ifndef AQR_NORM_MINB
-#define AQR_NORM_MINB 4
+#ifndef AQR_NORM_GRID_HP
+#define AQR_NORM_GRID_HP (148 * 4)
 #endif
-constexpr int kNormMinBlocks = AQR_NORM_MINB;
-__host__ __device__ inline int64_t norm_tiles(int64_t m) {
+constexpr int kNormGridHA = AQR_NORM_GRID_HA;
+constexpr int kNormGridHP = AQR_NORM_GRID_HP;
+constexpr int kNormGridMax = kNormGridHA > kNormGridHP ? kNormGridHA : kNormGridHP;
+__host__ __device__ inline int64_t norm_tiles(int64_t m, bool hp) {
     const int64_t b = (m + kBlock - 1) / kBlock;
-    return b < kNormGrid ? b : kNormGrid;
+    const int64_t g = hp ? kNormGridHP : kNormGridHA;
+    return b < g ? b : g;
 }
 
 // Programmatic dependent launch (sm_90+): a kernel launched with the
@@ -73,6 +76,24 @@ __host__ __device__ inline int64_t norm_tiles(int64_t m) {
 // launch.  Both are no-ops for ordinary launches.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Diagnostics (compiled in with -DAQR_TRACE): per-launch first-CTA start /
+// last-CTA end from %globaltimer, to measure the gaps between kernels.
+#ifdef AQR_TRACE
+__device__ unsigned long long *g_trace = nullptr;  // [slot][3]: pre-wait start, start, end
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_mark(int32_t slot, int which) {
+    if (slot < 0 || g_trace == nullptr || threadIdx.x != 0) return;
+    if (which < 2) atomicMin(g_trace + 3 * slot + which, gtimer());
+    else atomicMax(g_trace + 3 * slot + 2, gtimer());
+}
+#else
+__device__ __forceinline__ void trace_mark(int32_t, int) {}
+#endif
 
 __device__ __forceinline__ bool failed(const int32_t *status) {
     return status != nullptr && *(volatile const int32_t *)status >= 0;
@@ -335,15 +356,21 @@ struct ColArgs {
     const double *xnorm;  // x used for the norm partials when x == nullptr
     NormOut out;          // out.npart == nullptr: update only
     RrowIn rin;           // deferred r-row totals (rin.partial == nullptr: none)
+    int32_t trace;        // AQR_TRACE builds: launch slot (-1 off)
 };
 
 // Column update (+ norm chains when out.npart): launched with exactly
-// norm_tiles(m) CTAs (the canonical norm grid); kColTiles owned blocks are
+// norm_tiles(m, hp) CTAs (the canonical norm grid of the variant); kColTiles owned blocks are
 // processed per iteration with all their loads in flight, rows accumulated
 // in ascending block order.
-constexpr int kColTiles = 4;
-__global__ void __launch_bounds__(kBlock, kNormMinBlocks) col_update_norm_kernel(ColArgs a) {
+#ifndef AQR_COL_TILES
+#define AQR_COL_TILES 4
+#endif
+constexpr int kColTiles = AQR_COL_TILES;
+__global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
+    trace_mark(a.trace, 0);
     pdl_wait();
+    trace_mark(a.trace, 1);
     if (failed(a.out.status)) return;
     const bool upd = a.r != nullptr;
     const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
@@ -386,6 +413,7 @@ __global__ void __launch_bounds__(kBlock, kNormMinBlocks) col_update_norm_kernel
         norm_last_cta(a.out, gridDim.x);
     }
     rrow_rest(a.rin, blockIdx.x, gridDim.x);
+    trace_mark(a.trace, 2);
 }
 
 // Standalone totals of the norm partials (step API / multi-GPU driver).
@@ -480,6 +508,7 @@ struct TrailArgs {
     unsigned *counters;   // per group; nullptr: no in-kernel totals
     double *rout;         // totals: rout[j - jbeg] (row i of Rt from column jbeg)
     const int32_t *status;
+    int32_t trace;        // AQR_TRACE builds: launch slot (-1 off)
 };
 
 // Load the step vectors of one tile into registers; group 0 stores q_i/p_i.
@@ -581,10 +610,13 @@ __device__ __forceinline__ void trail_body(const TrailArgs &a, int tile, int gro
 
 template <int RPT, int CU, bool HP, bool CGS>
 __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
+    trace_mark(a.trace, 0);
     pdl_wait();
+    trace_mark(a.trace, 1);
     if (failed(a.status)) return;
     extern __shared__ double wsum[];  // [kWarps][cpg]
     trail_body<RPT, CU, HP, CGS>(a, blockIdx.x, blockIdx.y, wsum);
+    trace_mark(a.trace, 2);
     // totals: the next step's norm kernel (RrowIn) or rrow_reduce_kernel
 }
 
@@ -941,6 +973,7 @@ struct CsrArgs {
     double *znew;     // updated z_i (own rows)
     NormOut out;      // out.npart == nullptr: plain apply
     RrowIn rin;       // fused step: deferred r-row totals (partial == nullptr: none)
+    int32_t trace;    // AQR_TRACE builds: launch slot (-1 off)
 };
 
 // sum_q data[q] * xe(indices[q]) over q in [s, e), xe = x - rj qprev (upd),
@@ -1085,16 +1118,110 @@ __device__ __forceinline__ void csr_step_body(const CsrArgs &a, int64_t cta, int
     norm_last_cta(a.out, (unsigned)G);
 }
 
+// Software-pipelined variant: while the gathers of row r are in flight, the
+// (index, value) entries of row r + G*256 and the pointers of the row after
+// it are already loading, so each row costs one dependent round trip instead
+// of two.  Same rows, order and arithmetic as csr_step_body (bitwise equal).
+template <int B>
+__device__ __forceinline__ void load_entries(const CsrArgs &a, int s, int e, int (&c)[B], double (&v)[B]) {
+#pragma unroll
+    for (int h = 0; h < B; ++h) {
+        const bool ok = s + h < e;
+        c[h] = ok ? __ldg(a.indices + s + h) : 0;
+        v[h] = ok ? __ldg(a.data + s + h) : 0.0;
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void csr_step_body_pf(const CsrArgs &a, int64_t cta, int64_t G) {
+    const bool upd = a.r != nullptr;
+    const int64_t nblk = (a.m + kBlock - 1) / kBlock;
+    const int64_t stride = G * kBlock;
+    double t = 0.0, zz = 0.0, xx = 0.0;
+    int64_t row = cta * kBlock + threadIdx.x;
+    int s = row < a.m ? __ldg(a.indptr + row) : 0;
+    int e = row < a.m ? __ldg(a.indptr + row + 1) : 0;
+    int64_t nrow = row + stride;
+    int ns = nrow < a.m ? __ldg(a.indptr + nrow) : 0;
+    int ne = nrow < a.m ? __ldg(a.indptr + nrow + 1) : 0;
+    int c[B];
+    double v[B];
+    load_entries<B>(a, s, e, c, v);
+    const double rj = a.rin.partial ? rrow_first(a.rin, cta == 0) : (upd ? *a.r : 0.0);
+    for (int64_t blk = cta; blk < nblk; blk += G) {
+        // stage 1: pointers two rows ahead; stage 2: entries one row ahead
+        const int64_t n2 = nrow + stride;
+        const int s2 = n2 < a.m ? __ldg(a.indptr + n2) : 0;
+        const int e2 = n2 < a.m ? __ldg(a.indptr + n2 + 1) : 0;
+        int nc[B];
+        double nv[B];
+        load_entries<B>(a, ns, ne, nc, nv);
+        if (row < a.m) {
+            double y;
+            if (e - s <= B) {  // stage 3: gathers and the stored-order sum of this row
+                double xv[B];
+#pragma unroll
+                for (int h = 0; h < B; ++h) {
+                    const bool ok = s + h < e;
+                    xv[h] = ok ? __ldg(a.X + c[h]) : 0.0;
+                    if (upd && ok) xv[h] = __dsub_rn(xv[h], __dmul_rn(rj, __ldg(a.qprev + c[h])));
+                }
+                y = 0.0;
+#pragma unroll
+                for (int h = 0; h < B; ++h)
+                    if (s + h < e) y = __dadd_rn(y, __dmul_rn(v[h], xv[h]));
+            } else {
+                y = csr_row<B>(a, a.X, s, e, upd, rj);
+            }
+            double z = a.X[row];
+            if (upd) z = __dsub_rn(z, __dmul_rn(rj, a.qprev[row]));
+            a.Y[row] = y;
+            if (a.znew) a.znew[row] = z;
+            t = fma(z, y, t);
+            zz = fma(z, z, zz);
+            xx = fma(y, y, xx);
+        }
+        row = nrow;
+        s = ns;
+        e = ne;
+        nrow = n2;
+        ns = s2;
+        ne = e2;
+#pragma unroll
+        for (int h = 0; h < B; ++h) {
+            c[h] = nc[h];
+            v[h] = nv[h];
+        }
+    }
+    pdl_trigger();
+    norm_cta_partial(a.out, t, zz, xx, cta);
+    norm_last_cta(a.out, (unsigned)G);
+}
+
+template <int B, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) csr_step_pf_kernel(CsrArgs a) {
+    trace_mark(a.trace, 0);
+    pdl_wait();
+    trace_mark(a.trace, 1);
+    if (failed(a.out.status)) return;
+    csr_step_body_pf<B>(a, blockIdx.x, gridDim.x);
+    rrow_rest(a.rin, blockIdx.x, gridDim.x);
+    trace_mark(a.trace, 2);
+}
+
 // Fused HA/naive step, launched with exactly norm_tiles(m) CTAs (the
 // canonical norm grid): CTA b handles rows of the 256-row blocks b, b+G, ...
 // one per thread, accumulating the norm chains in ascending block order; the
 // next row's pointers are prefetched; one block tree per CTA at the end.
 template <int B, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) csr_step_kernel(CsrArgs a) {
+    trace_mark(a.trace, 0);
     pdl_wait();
+    trace_mark(a.trace, 1);
     if (failed(a.out.status)) return;
     csr_step_body<B>(a, blockIdx.x, gridDim.x);
     rrow_rest(a.rin, blockIdx.x, gridDim.x);
+    trace_mark(a.trace, 2);
 }
 
 // ---------------------------------------------------------------------------

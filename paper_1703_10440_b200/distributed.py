@@ -344,7 +344,8 @@ class CudaStepEngine:
             self.m, self._col(self.W, i), None, self._col(self.X, i) if hp else None, None, None,
             None if hp else self.xvec.data_ptr(), self.npart.data_ptr(), self.status.data_ptr(),
             D.stream_ptr()), "norm_partials")
-        self._chk(self.L.aqr_step_norm_reduce(self.m, self.npart.data_ptr(), self.tot.data_ptr(),
+        self._chk(self.L.aqr_step_norm_reduce(self.m, _lib.VARIANT_CODE[self.variant], self.npart.data_ptr(),
+                                              self.tot.data_ptr(),
                                               self.status.data_ptr(), D.stream_ptr()), "norm_reduce")
         return self.tot
 
