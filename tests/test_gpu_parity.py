@@ -340,3 +340,51 @@ def test_large_numpy_input_staged_h2d_bitwise(aqr):
     assert isinstance(r.Q, np.ndarray) and r.Q.flags.f_contiguous and r.Q.shape == (m, n)
     assert np.array_equal(r.Q, rd.Q.cpu().numpy()) and np.array_equal(r.R, rd.R.cpu().numpy())
     assert np.array_equal(Z, Z0)
+
+
+@pytest.mark.parametrize("chunk", [0, 1, 2])
+def test_pipeline_breakdown_and_edges(aqr, chunk, monkeypatch):
+    """Host-input pipeline edge cases: a breakdown in a late chunk (same
+    column, value and mv_count as the device call), n = 1, m = n, and a
+    callback operator."""
+    import torch
+
+    from paper_1703_10440_b200 import problems
+
+    monkeypatch.setenv("AQR_CHUNK_COLS", str(chunk))
+    ip, ix, dv = problems.laplacian5(40, 30, 1e-2)
+    m, n = 1200, 9
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    Z = np.asfortranarray(problems.rng(9, 4).standard_normal((m, n)))
+    Z[:, 6] = 0.0  # breakdown at column 6 (t = 0 exactly)
+    for meth in ("mgs-ha-row", "mgs-hp-row", "mgs-naive-row"):
+        got = []
+        for Zin in (Z, torch.from_numpy(Z.T).cuda().t()):
+            o = aqr.CsrSpdOperator(ip, ix, dv)
+            with pytest.raises(aqr.BreakdownError) as info:
+                aqr.factorize(Zin, o, meth)
+            got.append((info.value.column, info.value.value, o.mv_count))
+        assert got[0] == got[1], (meth, got)
+        assert got[0][0] == 6, (meth, got)
+    # n = 1 and m = n
+    for Zs in (Z[:, :1], np.asfortranarray(problems.rng(9, 5).standard_normal((8, 8)))):
+        A = np.eye(Zs.shape[0]) * 2.0 + 0.1
+        dop = aqr.DenseSpdOperator(A)
+        for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-naive-row"):
+            a = aqr.factorize(np.asfortranarray(Zs), dop, meth)
+            b = aqr.factorize(torch.from_numpy(np.ascontiguousarray(Zs.T)).cuda().t(), dop, meth)
+            assert np.array_equal(a.Q, b.Q.cpu().numpy()) and np.array_equal(a.R, b.R.cpu().numpy()), meth
+
+    # callback route (user SpdOperator) through the pipeline
+    class HostOp(aqr.SpdOperator):
+        def __init__(self):
+            super().__init__(m)
+
+        def _apply_into(self, x, y):
+            y[:] = O.csr_matvec(ip, ix, dv, x)
+
+    Zc = np.asfortranarray(problems.rng(9, 6).standard_normal((m, n)))
+    for meth in ("mgs-ha-row", "mgs-hp-row"):
+        a = aqr.factorize(Zc, HostOp(), meth)
+        b = aqr.factorize(Zc, op, meth)
+        assert np.array_equal(a.Q, b.Q) and np.array_equal(a.R, b.R), meth
