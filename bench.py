@@ -390,7 +390,10 @@ def run_b200_distributed(args, rank, world, local_rank):
             "data": "synthetic (seeded 5-pt Laplacian + N(0,1) Z; no dataset named by the reference)",
             "config": {"workload": "config2 row-partitioned: 5-pt Laplacian 1024^2 + 1e-2 I (CSR), "
                                    "Z 1048576x64 N(0,1)", "method": args.method, "m": m, "n": n,
-                       "parallelism": f"rows/{world} (NCCL all-reduce per step, SpMV halo exchange)",
+                       "parallelism": (f"rows/{world} (peer memory: halo reads and both per-step all-reduces "
+                                       f"fused into the step kernels over NVLink)"
+                                       if args.method.split("-")[1] in ("ha", "hp")
+                                       else f"rows/{world} (NCCL all-reduce per step, SpMV halo exchange)"),
                        "l2": "inputs larger than L2, no flush"},
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "roofline": None, "cpu_baseline": None, "e2e": e2e, "clocks": clocks.summary(),

@@ -236,6 +236,44 @@ AQR_API aqr_status aqr_step_finalize_r(int64_t n, const double *Rt, double *R, i
 AQR_API uint64_t aqr_status_bytes(int64_t n);
 AQR_API aqr_status aqr_status_init(int32_t *status, int64_t n, void *stream);
 
+/* ---- multi-GPU: exchanges fused into the step kernels over peer memory ---
+ * One process per GPU; the rows of Z and of the CSR operator are
+ * block-partitioned.  Each rank owns a working matrix W (m_loc x n, the Q
+ * output) and an exchange buffer, both allocated with aqr_p2p_alloc and
+ * mapped into every other rank with CUDA IPC (aqr_ipc_handle / aqr_ipc_open;
+ * the Python group in paper_1703_10440_b200/p2p.py does the collective
+ * handle exchange).  The halo of the local CSR block is read straight from
+ * the owning rank's W; the two all-reduces of every step are stores into all
+ * ranks' exchange buffers plus release/acquire flags, summed in rank order
+ * (bitwise equal on every rank; with one rank bitwise the single-GPU
+ * aqr_gs_factor).  Row orientation, HA or HP, MGS or CGS, CSR operators. */
+#define AQR_MAX_RANKS 8
+typedef struct aqr_p2p_group {
+    int32_t nranks, rank;
+    double *xbuf[AQR_MAX_RANKS];     /* exchange buffers (own pointer + peer mappings) */
+    const double *W[AQR_MAX_RANKS];  /* working matrices of every rank (own = args->Q) */
+    int64_t ldw[AQR_MAX_RANKS];
+    /* local CSR column m_loc + h (the halo) is row halo_row[h] of rank halo_rank[h] */
+    int64_t n_halo;
+    const int32_t *halo_rank, *halo_row; /* device */
+    uint64_t seq0; /* flag epoch: advance by n + 2 per factorization, same on all ranks */
+} aqr_p2p_group;
+
+/* Bytes of one rank's exchange buffer for n columns. */
+AQR_API uint64_t aqr_p2p_exchange_bytes(int64_t n);
+/* cudaMalloc'd, zeroed device memory that can be IPC-mapped. */
+AQR_API aqr_status aqr_p2p_alloc(uint64_t bytes, void **out);
+AQR_API aqr_status aqr_p2p_free(void *ptr);
+/* 64-byte CUDA IPC handle of an aqr_p2p_alloc block; open / close a peer's. */
+AQR_API aqr_status aqr_ipc_handle(const void *ptr, uint8_t out[64]);
+AQR_API aqr_status aqr_ipc_open(const uint8_t handle[64], void **out);
+AQR_API aqr_status aqr_ipc_close(void *ptr);
+/* The row-partitioned factorization of this rank's rows.  args: m = local
+ * rows, Q = group->W[rank] (ld = ldw[rank]), op = the local CSR block over
+ * m_loc + n_halo extended columns; R (replicated) is written on every rank.
+ * Collective: every rank calls it with the same n, method and seq0. */
+AQR_API aqr_status aqr_p2p_gs_factor(aqr_factor_args *args, const aqr_p2p_group *group, void *stream);
+
 /* ---- instrumentation (bench.py) ------------------------------------------
  * aqr_launch_count: number of kernels this library has launched so far in
  * the process (monotonic; read before/after a timed region).

@@ -57,10 +57,29 @@ class AqrFactorArgs(ctypes.Structure):
     ]
 
 
+MAX_RANKS = 8
+
+
+class AqrP2PGroup(ctypes.Structure):
+    _fields_ = [
+        ("nranks", c_i32), ("rank", c_i32),
+        ("xbuf", c_vp * MAX_RANKS), ("W", c_vp * MAX_RANKS), ("ldw", c_i64 * MAX_RANKS),
+        ("n_halo", c_i64), ("halo_rank", c_vp), ("halo_row", c_vp),
+        ("seq0", c_u64),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/aqr_b200.h
 SIGNATURES = {
     "aqr_workspace_bytes": (c_u64, [c_i32, c_i32, c_i32, c_i64, c_i64]),
     "aqr_gs_factor": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp]),
+    "aqr_p2p_exchange_bytes": (c_u64, [c_i64]),
+    "aqr_p2p_alloc": (c_i32, [c_u64, ctypes.POINTER(c_vp)]),
+    "aqr_p2p_free": (c_i32, [c_vp]),
+    "aqr_ipc_handle": (c_i32, [c_vp, ctypes.c_char_p]),
+    "aqr_ipc_open": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_vp)]),
+    "aqr_ipc_close": (c_i32, [c_vp]),
+    "aqr_p2p_gs_factor": (c_i32, [ctypes.POINTER(AqrFactorArgs), ctypes.POINTER(AqrP2PGroup), c_vp]),
     "aqr_trace_read": (c_i64, [c_vp, c_i64]),
     "aqr_gs_factor_d2h": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_gs_factor_pinned": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,

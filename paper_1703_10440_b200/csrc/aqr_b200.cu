@@ -25,6 +25,7 @@
 
 #include "../../include/aqr_b200.h"
 #include "aqr_kernels.cuh"
+#include "aqr_p2p.cuh"
 
 namespace {
 
@@ -849,6 +850,25 @@ struct Run {
     }
 };
 
+template <bool HP, bool CGS>
+aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, int64_t i, double *rii,
+                               int32_t *status, cudaStream_t s) {
+    aqr::TrailArgs a = a0;
+    const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
+    a.cpg = choose_cpg_generic(a.ntiles, ncols);
+    a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
+    dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
+    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
+    if (aqr::rows_per_thread(a.m) == 8) {
+        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, 2, HP, CGS>, smem));
+        launch_pdl(aqr::p2p_trailing_kernel<8, 2, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
+    } else {
+        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, smem));
+        launch_pdl(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
+    }
+    return launched("p2p_trailing_kernel");
+}
+
 }  // namespace
 
 extern "C" {
@@ -1133,6 +1153,207 @@ aqr_status aqr_gs_factor_d2h(aqr_factor_args *a, double *Q_host, int64_t ldqh, d
     if (cudaStreamSynchronize(S(stream)) != cudaSuccess && st == AQR_OK) st = set_err(AQR_ECUDA, "D2H R");
     side_release(sc);
     return st;
+}
+
+// ---- multi-GPU over peer memory (aqr_p2p.cuh) -------------------------------
+
+uint64_t aqr_p2p_exchange_bytes(int64_t n) { return 8 * (uint64_t)aqr::xb_words(std::max<int64_t>(n, 1)); }
+
+aqr_status aqr_p2p_alloc(uint64_t bytes, void **out) {
+    if (!out) return set_err(AQR_EARG, "null out");
+    *out = nullptr;
+    AQR_CUDA(cudaMalloc(out, std::max<uint64_t>(bytes, 256)));
+    AQR_CUDA(cudaMemset(*out, 0, std::max<uint64_t>(bytes, 256)));
+    return AQR_OK;
+}
+
+aqr_status aqr_p2p_free(void *ptr) {
+    if (ptr) AQR_CUDA(cudaFree(ptr));
+    return AQR_OK;
+}
+
+aqr_status aqr_ipc_handle(const void *ptr, uint8_t out[64]) {
+    cudaIpcMemHandle_t h;
+    AQR_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+    std::memcpy(out, &h, 64);
+    return AQR_OK;
+}
+
+aqr_status aqr_ipc_open(const uint8_t handle[64], void **out) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    AQR_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+    return AQR_OK;
+}
+
+aqr_status aqr_ipc_close(void *ptr) {
+    if (ptr) AQR_CUDA(cudaIpcCloseMemHandle(ptr));
+    return AQR_OK;
+}
+
+aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *stream) {
+    if (!a || !g) return set_err(AQR_EARG, "null args");
+    a->fail_col = -1;
+    a->fail_val = 0.0;
+    a->mv_count = 0;
+    const int64_t m = a->m, n = a->n;
+    if (g->nranks < 1 || g->nranks > aqr::kMaxRanks || g->rank < 0 || g->rank >= g->nranks)
+        return set_err(AQR_EARG, "bad group");
+    if (a->orientation != AQR_ROW || (a->variant != AQR_HA && a->variant != AQR_HP) || a->family < 0 ||
+        a->family > 1)
+        return set_err(AQR_EARG, "peer-memory path: row orientation, HA or HP");
+    if (!a->op || a->op->kind != AQR_OP_CSR || a->op->m != m)
+        return set_err(AQR_EARG, "peer-memory path: local CSR operator with m = local rows");
+    if (n < 1 || m < 1) return set_err(AQR_EDIM, "empty local block");
+    if (a->Q != g->W[g->rank] || a->ldq != g->ldw[g->rank] || a->ldq < m || !a->Z || a->ldz < m || !a->R ||
+        a->ldr < n)
+        return set_err(AQR_EARG, "Q must be the group's working matrix of this rank");
+    if (g->n_halo > 0 && (!g->halo_rank || !g->halo_row)) return set_err(AQR_EARG, "halo tables missing");
+    const Layout L = layout(a->family, a->variant, AQR_ROW, m, n);
+    if (!a->workspace || a->workspace_bytes < L.total)
+        return set_err(AQR_ENOMEM, "workspace smaller than aqr_workspace_bytes()");
+    const bool hp = a->variant == AQR_HP, cgs = a->family == AQR_CGS;
+    cudaStream_t s = S(stream);
+    void *ws = a->workspace;
+    int32_t *status = at<int32_t>(ws, L.status);
+    unsigned *counters = at<unsigned>(ws, L.counters);
+    double *Rt = at<double>(ws, L.rt), *partial = at<double>(ws, L.partial), *npart = at<double>(ws, L.npart);
+    double *xvec = at<double>(ws, L.xvec), *zvec = at<double>(ws, L.zvec), *pring = at<double>(ws, L.pring);
+    double *X = at<double>(ws, L.X), *Z0 = at<double>(ws, L.Z0);
+    double *W = a->Q;
+    const int64_t ldw = a->ldq;
+    auto col = [&](double *B, int64_t ld, int64_t j) { return B + j * ld; };
+
+    aqr::P2PArgs P;
+    std::memset(&P, 0, sizeof P);
+    P.nranks = g->nranks;
+    P.rank = g->rank;
+    for (int r = 0; r < g->nranks; ++r) {
+        P.xb[r] = g->xbuf[r];
+        P.W[r] = g->W[r];
+        P.ldw[r] = g->ldw[r];
+    }
+    P.n = n;
+    P.seq0 = g->seq0;
+    P.m_loc = m;
+    P.halo_rank = g->halo_rank;
+    P.halo_row = g->halo_row;
+
+    if (a->Z != a->Q) AQR_CUDA(copy_cols(a->Q, a->ldq, a->Z, a->ldz, m, n, cudaMemcpyDeviceToDevice, s));
+    AQR_TRY(aqr_status_init(status, n, stream));
+    AQR_CUDA(cudaMemsetAsync(counters, 0, 4 * (size_t)(n + 8), s));
+    AQR_CUDA(cudaMemsetAsync(Rt, 0, 8 * (size_t)n * n, s));
+    if (cgs) AQR_CUDA(copy_cols(Z0, m, a->Q, a->ldq, m, n, cudaMemcpyDeviceToDevice, s));
+    aqr::p2p_barrier_kernel<<<1, 1, 0, s>>>(P);  // this rank's Z is in place
+    AQR_TRY(launched("p2p_barrier_kernel"));
+    const aqr_op *op = a->op;
+    aqr::CsrArgs c;
+    std::memset(&c, 0, sizeof c);
+    c.m = m;
+    c.indptr = op->indptr;
+    c.indices = op->indices;
+    c.data = op->data;
+    c.trace = -1;
+    int64_t mv = 0;
+    if (hp) {  // X = op.apply_block(Zw), halo columns from the owners
+        aqr::CsrArgs b = c;
+        b.k = n;
+        b.X = W;
+        b.ldx = ldw;
+        b.Y = X;
+        b.ldy = m;
+        const int64_t nb = (m + aqr::kBlock - 1) / aqr::kBlock;
+        aqr::p2p_csr_block_kernel<<<(unsigned)std::min<int64_t>(nb, (int64_t)sm_count() * 8), aqr::kBlock, 0, s>>>(b, P);
+        AQR_TRY(launched("p2p_csr_block_kernel"));
+        mv += n;
+    }
+    const int32_t ntiles = (int32_t)aqr::num_tiles(m);
+    for (int64_t i = 0; i < n; ++i) {
+        aqr::NormOut o;
+        std::memset(&o, 0, sizeof o);
+        o.npart = npart;
+        o.ntiles = (int32_t)aqr::norm_tiles(m, hp);
+        o.counter = counters;
+        o.step = i;
+        o.status = status;
+        const unsigned gn = (unsigned)aqr::norm_tiles(m, hp);
+        if (hp) {
+            aqr::ColArgs ca;
+            std::memset(&ca, 0, sizeof ca);
+            ca.m = m;
+            ca.z = col(W, ldw, i);
+            ca.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+            ca.x = col(X, m, i);
+            ca.pprev = i > 0 ? pring + ((i - 1) & 1) * m : nullptr;
+            ca.out = o;
+            ca.trace = -1;
+            launch_pdl(aqr::p2p_col_update_kernel, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
+            AQR_TRY(launched("p2p_col_update_kernel"));
+        } else {
+            aqr::CsrArgs ca = c;
+            ca.k = 1;
+            ca.X = col(W, ldw, i);
+            ca.ldx = m;
+            ca.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+            ca.Y = xvec;
+            ca.ldy = m;
+            ca.znew = zvec;
+            ca.out = o;
+            if (op->max_row_nnz >= 1 && op->max_row_nnz <= 5)
+                launch_pdl(aqr::p2p_csr_step_kernel<5>, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
+            else
+                launch_pdl(aqr::p2p_csr_step_kernel<8>, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
+            AQR_TRY(launched("p2p_csr_step_kernel"));
+            ++mv;
+        }
+        aqr::TrailArgs t;
+        std::memset(&t, 0, sizeof t);
+        t.m = m;
+        t.ntiles = ntiles;
+        t.jbeg = (int32_t)(i + 1);
+        t.jend = (int32_t)n;
+        t.W = W;
+        t.ldw = ldw;
+        t.X = X;
+        t.ldx = m;
+        t.Z0 = Z0;
+        t.ldz0 = m;
+        t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+        t.pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
+        t.rprev = i > 0 ? Rt + (i - 1) * n : nullptr;
+        t.psrc = hp ? col(X, m, i) : xvec;
+        t.zsrc = hp ? col(W, ldw, i) : zvec;
+        t.qout = col(W, ldw, i);
+        t.pout = hp ? pring + (i & 1) * m : nullptr;
+        t.partial = partial;
+        t.status = status;
+        t.trace = -1;
+        aqr_status st;
+        if (hp) st = cgs ? launch_p2p_trailing<true, true>(t, P, i, Rt + i * n + i, status, s)
+                         : launch_p2p_trailing<true, false>(t, P, i, Rt + i * n + i, status, s);
+        else st = cgs ? launch_p2p_trailing<false, true>(t, P, i, Rt + i * n + i, status, s)
+                      : launch_p2p_trailing<false, false>(t, P, i, Rt + i * n + i, status, s);
+        AQR_TRY(st);
+        if (i + 1 < n) {
+            aqr::p2p_rrow_kernel<<<(unsigned)(n - 1 - i), aqr::kBlock, 0, s>>>(partial, ntiles, i + 1, P, i,
+                                                                          counters + 1, status);
+            AQR_TRY(launched("p2p_rrow_kernel"));
+        }
+    }
+    aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, Rt, a->R, a->ldr);
+    AQR_TRY(launched("finalize_r_kernel"));
+    std::vector<int32_t> st((16 + 4 * n) / 4);
+    AQR_CUDA(cudaMemcpyAsync(st.data(), status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
+    AQR_CUDA(cudaStreamSynchronize(s));
+    a->mv_count = mv;
+    if (a->flagged_host) std::memcpy(a->flagged_host, st.data() + 4, 4 * n);
+    if (st[0] >= 0) {
+        a->fail_col = st[0];
+        std::memcpy(&a->fail_val, st.data() + 2, 8);
+        return set_err(AQR_EBREAKDOWN, "breakdown at column " + std::to_string(st[0]));
+    }
+    return AQR_OK;
 }
 
 aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientation, int64_t m,

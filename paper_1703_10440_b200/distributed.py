@@ -117,6 +117,11 @@ class DistCsrSpdOperator(SpdOperator):
                 slot[c] = pos
                 pos += 1
         self.n_ext = pos
+        # halo slot h (column m_loc + h) = local row halo_row[h] of rank halo_rank[h]
+        self.halo_rank = np.fromiter((p for p in sorted(need) for _ in need[p]), dtype=np.int32,
+                                     count=pos - m_loc)
+        self.halo_row = np.fromiter((c - self.partition[p][0] for p in sorted(need) for c in need[p]),
+                                    dtype=np.int32, count=pos - m_loc)
         local = indices - r0
         outside = (indices < r0) | (indices >= r1)
         if outside.any():
@@ -395,13 +400,16 @@ class CudaStepEngine:
         return self.W, R, fail, fail_val, [int(j) for j in np.flatnonzero(flags)]
 
 
-def dist_factorize(Z_local, op, method="mgs-ha-row", group=None, engine=None):
+def dist_factorize(Z_local, op, method="mgs-ha-row", group=None, engine=None, backend=None):
     """Row-partitioned factorization; every rank passes its row block.
 
     ``op`` is a DistCsrSpdOperator / DistDenseSpdOperator (collective
     applies).  Returns QrResult(Q_local, R (replicated), cost, flagged).
     Only the row-oriented schedule exists here; it is bitwise the single-GPU
-    result when world_size == 1.
+    result when world_size == 1.  HA / HP with a DistCsrSpdOperator run on
+    the peer-memory path (``p2p.py``: halo reads and both all-reduces fused
+    into the step kernels); ``backend="nccl"`` (or naive, or a dense
+    operator) runs the step-API engine below with NCCL all-reduces.
     """
     dist = _dist()
     if not isinstance(method, MethodId):
@@ -414,6 +422,15 @@ def dist_factorize(Z_local, op, method="mgs-ha-row", group=None, engine=None):
         raise DimensionError("local block does not match the operator")
     if op.global_dim < n:
         raise DimensionError(f"need m >= n >= 1, got m={op.global_dim}, n={n}")
+    from . import p2p
+
+    if backend not in (None, "p2p", "nccl"):
+        raise ValueError("backend must be 'p2p' or 'nccl'")
+    if engine is None and backend != "nccl" and p2p.supported(op, method):
+        # exchanges fused into the step kernels over peer memory (csrc/aqr_p2p.cuh)
+        return p2p.p2p_factorize(Z_local, op, method, group=group)
+    if backend == "p2p":
+        raise ValueError("the peer-memory path runs HA / HP row factorizations with a DistCsrSpdOperator")
     eng = engine or CudaStepEngine(m_loc, n, family, variant, Z_local.device)
     mv_before = op.mv_count
     eng.load(Z_local)
