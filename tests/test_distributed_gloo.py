@@ -59,6 +59,14 @@ def _worker(rank, world, port, case, method, outdir):
             ref = O.csr_matvec(ip, ix, dv, x)[r0:r1]
             assert np.array_equal(y.numpy(), ref)
             op.mv_count = 0
+            # the peer-memory halo tables name the owner and its local row of every halo column
+            gl = ix[ip[r0]:ip[r1]]
+            loc = op.indices_local
+            halo = loc >= (r1 - r0)
+            h = loc[halo] - (r1 - r0)
+            owner_start = np.array([part[p][0] for p in op.halo_rank[h]])
+            assert np.array_equal(owner_start + op.halo_row[h], gl[halo])
+            assert np.all(op.halo_rank != rank) and len(op.halo_rank) == op.n_ext - (r1 - r0)
         fam, var, _ = method.split("-")
         eng = E.CpuStepEngine(r1 - r0, n, fam, var)
         res = DD.dist_factorize(torch.from_numpy(np.asfortranarray(Z[r0:r1])), op, method, engine=eng)
