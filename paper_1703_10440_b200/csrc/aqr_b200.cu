@@ -315,10 +315,19 @@ aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx
         aqr::dense_gemv_kernel<<<grid, aqr::kGemvBlock, 0, s>>>(m, ncols, op->A, op->lda, X, ldx, Y, ldy);
         return launched("dense_gemv_kernel");
     }
-    dim3 grid((unsigned)((m + aqr::kGemmBM - 1) / aqr::kGemmBM),
-              (unsigned)((k + aqr::kGemmBN - 1) / aqr::kGemmBN));
-    aqr::dense_gemm_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
-    return launched("dense_gemm_kernel");
+    static const int gv = [] {  // AQR_GEMM_VARIANT=1: the 64 x 64 / 4 x 4 kernel (A/B)
+        const char *e = std::getenv("AQR_GEMM_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (gv == 1) {
+        dim3 grid((unsigned)((m + aqr::kGemmBM - 1) / aqr::kGemmBM),
+                  (unsigned)((k + aqr::kGemmBN - 1) / aqr::kGemmBN));
+        aqr::dense_gemm_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
+        return launched("dense_gemm_kernel");
+    }
+    dim3 grid((unsigned)((m + aqr::kG2BM - 1) / aqr::kG2BM), (unsigned)((k + aqr::kG2BN - 1) / aqr::kG2BN));
+    aqr::dense_gemm2_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
+    return launched("dense_gemm2_kernel");
 }
 
 aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,

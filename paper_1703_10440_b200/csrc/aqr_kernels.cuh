@@ -1398,4 +1398,79 @@ __global__ void __launch_bounds__(256)
         }
 }
 
+// Larger register tiles for the FP64 pipe: CTA 128 x 64 outputs, 256 threads,
+// 8 x 4 outputs per thread (12 shared loads per 64 FP64 instructions instead
+// of 8 per 32), the next 16-deep slice of A and X prefetched into registers
+// while the current one is consumed (double-buffered shared memory).  Same
+// per-output order (ascending j, separately rounded multiply and add).
+constexpr int kG2BM = 128, kG2BN = 64, kG2BK = 16;
+__global__ void __launch_bounds__(256, 1)
+    dense_gemm2_kernel(int64_t m, int64_t ncols, int64_t k, const double *__restrict__ A, int64_t lda,
+                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y, int64_t ldy) {
+    __shared__ double As[2][kG2BK][kG2BM];
+    __shared__ double Xs[2][kG2BK][kG2BN];  // 48 KB total with As (static limit)
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t i0 = (int64_t)blockIdx.x * kG2BM, c0 = (int64_t)blockIdx.y * kG2BN;
+    double acc[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    // per-thread load slots: A: 8 elements (rows tid & 127, slices (tid >> 7) + 2u),
+    // X: 4 elements (slice tid & 15, columns (tid >> 4) + 16u)
+    double ra[8], rx[4];
+    auto load = [&](int64_t j0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int ii = tid & 127, jj = (tid >> 7) + 2 * u;
+            const int64_t gi = i0 + ii, gj = j0 + jj;
+            ra[u] = (gi < m && gj < ncols) ? __ldg(A + gi + gj * lda) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int jj = tid & 15, cc = (tid >> 4) + 16 * u;
+            const int64_t gj = j0 + jj, gc = c0 + cc;
+            rx[u] = (gj < ncols && gc < k) ? __ldg(X + gj + gc * ldx) : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) As[buf][(tid >> 7) + 2 * u][tid & 127] = ra[u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Xs[buf][tid & 15][(tid >> 4) + 16 * u] = rx[u];
+    };
+    load(0);
+    store(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t j0 = 0; j0 < ncols; j0 += kG2BK) {
+        const bool more = j0 + kG2BK < ncols;
+        if (more) load(j0 + kG2BK);
+        const int kmax = (ncols - j0) < kG2BK ? (int)(ncols - j0) : kG2BK;
+        for (int jj = 0; jj < kmax; ++jj) {
+            double av[8], xv[4];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) av[a] = As[buf][jj][ty + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) xv[b] = Xs[buf][jj][tx + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(av[a], xv[b]));
+        }
+        if (more) {
+            store(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int64_t gi = i0 + ty + 16 * a, gc = c0 + tx + 16 * b;
+            if (gi < m && gc < k) Y[gi + gc * ldy] = acc[a][b];
+        }
+}
+
 }  // namespace aqr
