@@ -1,0 +1,64 @@
+"""Every kernel variant kept behind an experiment knob computes the same bits.
+
+The knobs are read once per process (include/aqr_b200.h, DESIGN.md section
+8), so each variant runs in a subprocess and its factors are compared
+bitwise with the default build's: the TMA-bulk trailing kernel (with and
+without the L2 hint), the unpipelined SpMV step, the separate R-row
+reduction launch, launches without programmatic dependent launch.
+"""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {repo!r})
+import paper_1703_10440_b200 as aqr
+from paper_1703_10440_b200 import problems
+ip, ix, dv = problems.laplacian5(700, 460, 1e-2)   # m = 322,000: the 2048-row tile path
+m, n = 700 * 460, 7
+Z = problems.rng(9, 7).standard_normal((n, m)).T
+Zd = torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().t()
+op = aqr.CsrSpdOperator(ip, ix, dv)
+out = {{}}
+for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "mgs-naive-row", "mgs-hp-col"):
+    r = aqr.factorize(Zd, op, meth)
+    out[meth + "|Q"] = r.Q.cpu().numpy()
+    out[meth + "|R"] = r.R.cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def _run(env_extra, path):
+    env = dict(os.environ)
+    env.update(env_extra)
+    code = SCRIPT.format(repo=REPO, path=str(path))
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    return np.load(path)
+
+
+@pytest.fixture(scope="module")
+def default_factors(tmp_path_factory):
+    return _run({}, tmp_path_factory.mktemp("v") / "default.npz")
+
+
+@pytest.mark.parametrize("knobs", [
+    {"AQR_TRAIL_VARIANT": "1"},
+    {"AQR_TRAIL_VARIANT": "4"},
+    {"AQR_TRAIL_VARIANT": "3"},
+    {"AQR_SPMV_VARIANT": "3"},
+    {"AQR_DEFER": "0"},
+    {"AQR_PDL": "0"},
+])
+def test_variant_bitwise_equal_default(default_factors, knobs, tmp_path):
+    got = _run(knobs, tmp_path / "variant.npz")
+    for key in default_factors.files:
+        assert np.array_equal(got[key], default_factors[key]), (knobs, key)
