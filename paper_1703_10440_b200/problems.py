@@ -164,3 +164,54 @@ def _out(csr, Z, device):
 
     indptr, indices, data = (torch.from_numpy(a).cuda() for a in csr)
     return (indptr, indices, data), torch.from_numpy(Z.T).cuda().t()
+
+
+# ---- the reference's testbed generators used by the bench / factor CLI ----
+
+def make_rng(seed):
+    """The reference's deterministic generator (testbed.py:29-31)."""
+    return np.random.default_rng(np.random.SeedSequence(seed))
+
+
+def haar_orthogonal(rng, k):
+    """Haar orthogonal k x k: QR of a Gaussian, column signs fixed (linalg.py:59-75)."""
+    from .exceptions import DimensionError
+
+    if k < 1:
+        raise DimensionError("k must be >= 1")
+    while True:
+        G = rng.standard_normal((k, k))
+        Q, R = np.linalg.qr(G)
+        d = np.diag(R)
+        if np.all(d != 0.0):
+            break
+    return np.asfortranarray(Q * np.where(d < 0.0, -1.0, 1.0))
+
+
+def build_spd(m, kappa, rng):
+    """(eigenvalues, DenseSpdOperator) with eigenvalues 10^(alpha (i-1)) (testbed.py:77-88).
+
+    A = (V diag(d)) V^T is formed by the bitwise sequential dense block apply
+    on the device (the reference's per-entry sequential matmul), then
+    symmetrized."""
+    from .exceptions import DimensionError
+    from .operators import DenseSpdOperator
+
+    if m < 2:
+        raise DimensionError("m must be >= 2")
+    if kappa < 1.0:
+        raise ValueError("kappa must be >= 1")
+    V = haar_orthogonal(rng, m)
+    d = 10.0 ** (np.log10(kappa) / (m - 1) * np.arange(m))
+    A = np.asarray(DenseSpdOperator(np.asfortranarray(V * d)).apply_block(np.asfortranarray(V.T)))
+    return d, DenseSpdOperator(np.asfortranarray(0.5 * (A + A.T)))
+
+
+def laplacian_spd(nx, ny):
+    """5-point Laplacian on an nx-by-ny grid, Dirichlet boundary, CSR (testbed.py:128-153)."""
+    from .exceptions import DimensionError
+    from .operators import CsrSpdOperator
+
+    if nx < 2 or ny < 2:
+        raise DimensionError("grid must be at least 2x2")
+    return CsrSpdOperator(*laplacian5(nx, ny, 0.0))
