@@ -364,9 +364,10 @@ aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, d
 aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, double *x,
                                   const double *pprev, const double *r, const double *xnorm,
                                   const aqr::NormOut &out, bool hp_grid, cudaStream_t s,
-                                  const aqr::RrowIn *rin = nullptr) {
+                                  const aqr::RrowIn *rin = nullptr, const double *zsrc = nullptr) {
     aqr::ColArgs a;
     std::memset(&a.rin, 0, sizeof a.rin);
+    a.zsrc = zsrc;
     a.trace = out.npart != nullptr ? trace_slot() : -1;
     if (rin) a.rin = *rin;
     a.m = m;
@@ -436,7 +437,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     // AQR_TRAIL_VARIANT: 0 = LDG CU=2 (default), 3 = LDG CU=4 (HA),
     // 1 = TMA without the L2 hint, 4 = TMA with the evict-first hint.
     const int tv = trail_variant();
-    const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && (tv == 1 || tv == 4);
+    const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && (tv == 1 || tv == 4) && a.Wsrc == nullptr;
     a.cpg = tma ? (int32_t)std::max<int64_t>(ncols, 1) : choose_cpg_generic(a.ntiles, ncols);
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
 
@@ -549,6 +550,14 @@ void side_release(const SideCtx &c) {
     g_side_free.push_back(c);
 }
 
+int direct_mode() {  // AQR_DIRECT=0: copy Z into Q first (A/B experiments)
+    static const int v = [] {
+        const char *e = std::getenv("AQR_DIRECT");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 int defer_mode() {  // AQR_DEFER=0: separate r-row reduction launch (A/B experiments)
     static const int v = [] {
         const char *e = std::getenv("AQR_DEFER");
@@ -643,6 +652,17 @@ struct Run {
     HostOut *ho = nullptr;
     Pipe *pp = nullptr;
     int64_t live = 0;  // columns [0, live) are resident and caught up
+    // Direct mode (row form, Z distinct from Q): the input Z is read in place
+    // by steps 0 and 1 -- the first writes of the trailing columns happen in
+    // the trailing pass of step 1 -- so the copy Zw = Z (gram_schmidt.py:131)
+    // is never materialized; CGS dots use Z itself as Z0.
+    const double *Zin = nullptr;
+    int64_t ldzin = 0;
+    const double *Z0p = nullptr;
+    int64_t ldz0 = 0;
+    const double *zread(int64_t j, int64_t step) const {
+        return (Zin && step <= 1) ? Zin + j * ldzin : nullptr;
+    }
     cudaStream_t s;
     bool hp, cgs, naive, csr_native;
     int64_t m, n;
@@ -740,31 +760,37 @@ struct Run {
         const aqr::RrowIn rin = rrow_in(j);
         const aqr::RrowIn *pin = pending ? &rin : nullptr;
         pending = false;
+        const double *zs = zread(j, j);  // column j as read at step j (nullptr: W)
         if (hp) {
             double *x = col(X, m, j);
-            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), true, s, pin));
-            zcol = z;
+            AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), true, s, pin, zs));
+            zcol = (zs && !r) ? zs : z;  // without an update nothing was written to W
             xcol = x;
         } else if (csr_native) {
             // one fused launch: r_{j-1,j} (and the rest of row j-1 of R),
             // gather (z - r q), x = A z, z_new, norm, r_jj
             double *xo = xout(j);
-            AQR_TRY(launch_csr(a->op, 1, z, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
+            const double *zx = zs ? zs : z;
+            AQR_TRY(launch_csr(a->op, 1, zx, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
             static const int rep = [] {  // diagnostics: idempotent repeats of the step
                 const char *e = std::getenv("AQR_SPMV_REPEAT");
                 return e ? std::atoi(e) : 0;
             }();
             for (int k = 0; k < rep; ++k)
-                AQR_TRY(launch_csr(a->op, 1, z, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
+                AQR_TRY(launch_csr(a->op, 1, zx, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
             ++mv;
             zcol = zvec;
             xcol = xo;
         } else {
             double *xo = xout(j);
-            if (r) AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, no_norm(), false, s));
-            AQR_TRY(mv1(z, xo));  // op.apply(Zw[:, j].copy()), line 151
-            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xo, norm_out(j), false, s));
-            zcol = z;
+            if (r)
+                AQR_TRY(launch_col_update_norm(m, z, qprev, nullptr, nullptr, r, nullptr, no_norm(), false, s,
+                                               nullptr, zs));
+            const double *zr = (zs && !r) ? zs : z;  // the current z_j
+            AQR_TRY(mv1(zr, xo));  // op.apply(Zw[:, j].copy()), line 151
+            AQR_TRY(launch_col_update_norm(m, z, nullptr, nullptr, nullptr, nullptr, xo, norm_out(j), false, s,
+                                           nullptr, zr));
+            zcol = zr;
             xcol = xo;
         }
         return AQR_OK;
@@ -781,8 +807,10 @@ struct Run {
         t.ldw = ldw;
         t.X = X;
         t.ldx = m;
-        t.Z0 = Z0;
-        t.ldz0 = m;
+        t.Z0 = Z0p ? Z0p : Z0;
+        t.ldz0 = Z0p ? ldz0 : m;
+        t.Wsrc = zread(0, i);  // steps 0 and 1 read the input Z in place
+        t.ldwsrc = ldzin;
         t.rprev = i > 0 ? Rt + (i - 1) * n : nullptr;
         t.partial = partial;
         t.counters = counters + 1;
@@ -1017,15 +1045,24 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
     r.Z0 = at<double>(ws, L.Z0);
     cudaStream_t s = r.s;
 
-    if (a->Z != a->Q)  // Zw = Z.copy(order="F"), line 131
+    const bool direct = a->Z != a->Q && a->orientation == AQR_ROW && !r.pp && direct_mode() != 0;
+    if (direct) {  // Zw = Z.copy(order="F") (line 131) is read in place instead
+        r.Zin = a->Z;
+        r.ldzin = a->ldz;
+        if (r.cgs) {  // Z0 = Z (line 132): the input itself stays untouched
+            r.Z0p = a->Z;
+            r.ldz0 = a->ldz;
+        }
+    } else if (a->Z != a->Q) {  // Zw = Z.copy(order="F"), line 131
         AQR_CUDA(copy_cols(a->Q, a->ldq, a->Z, a->ldz, m, n, cudaMemcpyDeviceToDevice, s));
+    }
     AQR_TRY(aqr_status_init(r.status, n, stream));
     AQR_CUDA(cudaMemsetAsync(r.counters, 0, 4 * (size_t)(n + 8), s));
     AQR_CUDA(cudaMemsetAsync(r.Rt, 0, 8 * (size_t)n * n, s));
-    if (r.cgs && !r.pp)  // Z0, line 132 (per chunk when pipelined)
+    if (r.cgs && !r.pp && !direct)  // Z0, line 132 (per chunk when pipelined)
         AQR_CUDA(copy_cols(r.Z0, m, a->Q, a->ldq, m, n, cudaMemcpyDeviceToDevice, s));
     if (r.hp && !r.pp) {  // X = op.apply_block(Zw), line 136 (per chunk when pipelined)
-        AQR_TRY(op_apply(a->op, n, a->Q, a->ldq, r.X, m, s));
+        AQR_TRY(op_apply(a->op, n, direct ? a->Z : a->Q, direct ? a->ldz : a->ldq, r.X, m, s));
         r.mv += n;
     }
     static const bool debug_timing = std::getenv("AQR_DEBUG_TIMING") != nullptr;

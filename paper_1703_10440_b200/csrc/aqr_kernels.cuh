@@ -349,6 +349,7 @@ __device__ __forceinline__ void rrow_rest(const RrowIn &in, int64_t cta, int64_t
 struct ColArgs {
     int64_t m;
     double *z;
+    const double *zsrc;  // read z from here instead of z (nullptr: z); results go to z
     const double *qprev;
     double *x;  // HP: carried column, updated in place (nullptr otherwise)
     const double *pprev;
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
         for (int g = 0; g < kColTiles; ++g) {  // loads first
             const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
             const bool ok = b0 + g * G < nblk && r < a.m;
-            z[g] = ok ? a.z[r] : 0.0;
+            z[g] = ok ? (a.zsrc ? a.zsrc[r] : a.z[r]) : 0.0;
             q[g] = (ok && upd) ? a.qprev[r] : 0.0;
             xv[g] = ok ? (a.x ? a.x[r] : (a.xnorm ? a.xnorm[r] : 0.0)) : 0.0;
             pp[g] = (ok && upd && a.x) ? a.pprev[r] : 0.0;
@@ -492,6 +493,8 @@ struct TrailArgs {
     int32_t reverse;  // walk the work items backwards (L2 reuse across steps)
     double *W;
     int64_t ldw;
+    const double *Wsrc;  // read the trailing columns from here (nullptr: W); results go to W
+    int64_t ldwsrc;
     double *X;  // HP carried A z (nullptr otherwise)
     int64_t ldx;
     const double *Z0;  // CGS original columns (nullptr for MGS)
@@ -562,7 +565,7 @@ __device__ __forceinline__ void trail_body(const TrailArgs &a, int tile, int gro
             const int j = j0 + c;
             const bool cj = j < cend;
             rj[c] = (cj && upd) ? a.rprev[j] : 0.0;
-            const double *zc = a.W + (int64_t)j * a.ldw;
+            const double *zc = a.Wsrc ? a.Wsrc + (int64_t)j * a.ldwsrc : a.W + (int64_t)j * a.ldw;
 #pragma unroll
             for (int u = 0; u < RPT; ++u) {
                 const int64_t r = row0 + (int64_t)u * kBlock;

@@ -29,7 +29,7 @@ Z = problems.rng(9, 7).standard_normal((n, m)).T
 Zd = torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().t()
 op = aqr.CsrSpdOperator(ip, ix, dv)
 out = {{}}
-for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "mgs-naive-row", "mgs-hp-col"):
+for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "cgs-hp-row", "mgs-naive-row", "mgs-hp-col"):
     r = aqr.factorize(Zd, op, meth)
     out[meth + "|Q"] = r.Q.cpu().numpy()
     out[meth + "|R"] = r.R.cpu().numpy()
@@ -57,6 +57,7 @@ def default_factors(tmp_path_factory):
     {"AQR_SPMV_VARIANT": "3"},
     {"AQR_DEFER": "0"},
     {"AQR_PDL": "0"},
+    {"AQR_DIRECT": "0"},
 ])
 def test_variant_bitwise_equal_default(default_factors, knobs, tmp_path):
     got = _run(knobs, tmp_path / "variant.npz")
