@@ -126,3 +126,24 @@ def test_dense_gemv_path_parity(aqr):
         tq, tr = parity.tolerance(Z, ("dense", A), meth)
         eq, er = parity.factor_errors(r.Q, r.R, o.Q, o.R)
         assert eq <= tq and er <= tr, (meth, eq, tq, er, tr)
+
+
+def test_many_columns_invariants(aqr):
+    """n = 700 > every per-kernel column batch (TMA staging 256, group sizes):
+    col == row bitwise, triangular R, A-orthogonality."""
+    import torch
+
+    from paper_1703_10440_b200 import problems
+
+    ip, ix, dv = problems.laplacian5(120, 100, 1e-1)
+    m, n = 12000, 700
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    Zd = torch.from_numpy(problems.rng(9, 8).standard_normal((n, m))).cuda().t()
+    r = aqr.factorize(Zd, op, "mgs-hp-row")
+    c = aqr.factorize(Zd, op, "mgs-hp-col")
+    assert torch.equal(r.Q, c.Q) and torch.equal(r.R, c.R)
+    R = r.R.cpu().numpy()
+    assert np.array_equal(np.tril(R, -1), np.zeros_like(R)) and np.all(np.diag(R) > 0)
+    assert aqr.loss_of_A_orthogonality(r.Q, op) < 1e-12
+    h = aqr.factorize(Zd, op, "mgs-ha-row")
+    assert aqr.residual_rel(Zd, h.Q, h.R) < 1e-14
