@@ -550,6 +550,14 @@ void side_release(const SideCtx &c) {
     g_side_free.push_back(c);
 }
 
+int col_schedule_mode() {  // AQR_COL_SCHEDULE=1: the column-oriented loop for col orientation
+    static const int v = [] {
+        const char *e = std::getenv("AQR_COL_SCHEDULE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 int direct_mode() {  // AQR_DIRECT=0: copy Z into Q first (A/B experiments)
     static const int v = [] {
         const char *e = std::getenv("AQR_DIRECT");
@@ -1020,7 +1028,13 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
     Run r;
     r.a = a;
     r.ho = ho;
-    r.pp = (pp && a->orientation == AQR_ROW) ? pp : nullptr;
+    // Both orientations give bitwise-identical factors (same per-column
+    // sequence of updates, same reduction trees; tested), so the column
+    // orientation runs the row-oriented step schedule unless
+    // AQR_COL_SCHEDULE=1 asks for the column loop (n(n-1)/2 dependent global
+    // reductions: latency-bound, 27 vs 7.6 ms on config 2).
+    const bool row_sched = a->orientation == AQR_ROW || col_schedule_mode() == 0;
+    r.pp = (pp && row_sched) ? pp : nullptr;
     r.s = S(stream);
     r.hp = a->variant == AQR_HP;
     r.naive = a->variant == AQR_NAIVE;
@@ -1043,9 +1057,13 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
     r.P = at<double>(ws, L.P);
     r.X = at<double>(ws, L.X);
     r.Z0 = at<double>(ws, L.Z0);
+    if (row_sched && a->orientation == AQR_COL) {  // the row schedule's vectors live in P's storage
+        r.pvec = r.P;
+        r.pring = r.P;  // n >= 2: 2m <= mn; n = 1 uses slot 0 only
+    }
     cudaStream_t s = r.s;
 
-    const bool direct = a->Z != a->Q && a->orientation == AQR_ROW && !r.pp && direct_mode() != 0;
+    const bool direct = a->Z != a->Q && row_sched && !r.pp && direct_mode() != 0;
     if (direct) {  // Zw = Z.copy(order="F") (line 131) is read in place instead
         r.Zin = a->Z;
         r.ldzin = a->ldz;
@@ -1067,7 +1085,7 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
     }
     static const bool debug_timing = std::getenv("AQR_DEBUG_TIMING") != nullptr;
     const auto t_loop = std::chrono::steady_clock::now();
-    AQR_TRY(a->orientation == AQR_ROW ? r.row_form() : r.col_form());
+    AQR_TRY(row_sched ? r.row_form() : r.col_form());
     aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, r.Rt, a->R, a->ldr);
     AQR_TRY(launched("finalize_r_kernel"));
     std::vector<int32_t> st((16 + 4 * n) / 4);
@@ -1120,7 +1138,11 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
     cudaStream_t s = S(stream);
     a->Z = a->Q;  // Z is staged into Q (factorized in place)
     a->ldz = a->ldq;
-    if (a->orientation != AQR_ROW) {  // column form: whole H2D first, then the streamed D2H
+    // Whole H2D first, then the streamed D2H: for the column loop, and for HP
+    // with a user operator, whose apply_block must see all n columns in one
+    // call (gram_schmidt.py:136; the pipeline applies it chunk by chunk).
+    const bool hp_callback = a->variant == AQR_HP && a->op && a->op->kind == AQR_OP_CALLBACK;
+    if ((a->orientation != AQR_ROW && col_schedule_mode() != 0) || hp_callback) {
         AQR_CUDA(copy_cols(a->Q, a->ldq, Z_host, ldzh, m, n, cudaMemcpyHostToDevice, s));
         return aqr_gs_factor_d2h(a, Q_host, ldqh, R_host, ldrh, stream);
     }

@@ -130,6 +130,11 @@ def test_hp_uses_one_block_call(aqr, golden):
 
     op.apply_block, op.apply = spy_block, spy_apply
     ref_hp = None
+    for orientation in ("row", "col"):  # host-input pipeline and column orientation keep one block call
+        calls.clear()
+        aqr.mgs_hp(Z, op, orientation)
+        assert calls == [("block", n)], orientation
+    calls.clear()
     r = aqr.mgs_hp(Z, op)
     assert calls == [("block", n)]
     calls.clear()

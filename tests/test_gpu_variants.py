@@ -4,7 +4,9 @@ The knobs are read once per process (include/aqr_b200.h, DESIGN.md section
 8), so each variant runs in a subprocess and its factors are compared
 bitwise with the default build's: the TMA-bulk trailing kernel (with and
 without the L2 hint), the unpipelined SpMV step, the separate R-row
-reduction launch, launches without programmatic dependent launch.
+reduction launch, launches without programmatic dependent launch, the
+materialized copy of Z, and the column-oriented loop for the col methods
+(by default they run the row-oriented step schedule).
 """
 
 import os
@@ -29,7 +31,8 @@ Z = problems.rng(9, 7).standard_normal((n, m)).T
 Zd = torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().t()
 op = aqr.CsrSpdOperator(ip, ix, dv)
 out = {{}}
-for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "cgs-hp-row", "mgs-naive-row", "mgs-hp-col"):
+for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "cgs-hp-row", "mgs-naive-row", "mgs-hp-col",
+             "mgs-ha-col", "cgs-naive-col"):
     r = aqr.factorize(Zd, op, meth)
     out[meth + "|Q"] = r.Q.cpu().numpy()
     out[meth + "|R"] = r.R.cpu().numpy()
@@ -58,6 +61,7 @@ def default_factors(tmp_path_factory):
     {"AQR_DEFER": "0"},
     {"AQR_PDL": "0"},
     {"AQR_DIRECT": "0"},
+    {"AQR_COL_SCHEDULE": "1"},
 ])
 def test_variant_bitwise_equal_default(default_factors, knobs, tmp_path):
     got = _run(knobs, tmp_path / "variant.npz")

@@ -1,0 +1,30 @@
+"""Diagnostics: kernel timeline of the host-input pipeline (needs a -DAQR_TRACE
+build: AQR_LIB_PATH=build_ab/libaqr_trace.so)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1703_10440_b200 as aqr
+from paper_1703_10440_b200 import problems, _lib
+L = _lib.lib()
+(ip, ix, dv), Z = problems.config2(device=False)
+m, n = Z.shape
+op = aqr.CsrSpdOperator(ip, ix, dv)
+Zh = torch.empty((n, m), dtype=torch.float64).pin_memory().t(); Zh.copy_(torch.from_numpy(Z))
+meth = sys.argv[1] if len(sys.argv) > 1 else "mgs-ha-row"
+for _ in range(3):
+    r = aqr.factorize(Zh, op, meth)
+buf = np.zeros(3 * 16384, dtype=np.uint64)
+k0 = L.aqr_trace_read(buf.ctypes.data, 16384)
+t0 = time.perf_counter()
+r = aqr.factorize(Zh, op, meth)
+t1 = time.perf_counter()
+k = L.aqr_trace_read(buf.ctypes.data, 16384)
+t = buf[: 3 * k].reshape(k, 3)[k0:].astype(np.int64)
+start, end = t[:, 1], t[:, 2]
+base = start[0]
+print(f"{meth}: wall {1e3 * (t1 - t0):.2f} ms, {len(t)} traced launches, first start -> last end "
+      f"{(end[-1] - base) / 1e6:.2f} ms, busy {(end - start).sum() / 1e6:.2f} ms")
+# idle gaps > 20 us (waiting for H2D chunks)
+gaps = [(i, (start[i] - end[i - 1]) / 1e3, (start[i] - base) / 1e6) for i in range(1, len(t)) if start[i] - end[i - 1] > 20000]
+for i, g, at in gaps:
+    print(f"  idle {g:8.1f} us before launch {i} at {at:.2f} ms")
