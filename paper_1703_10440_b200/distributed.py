@@ -414,8 +414,10 @@ def dist_factorize(Z_local, op, method="mgs-ha-row", group=None, engine=None, ba
     dist = _dist()
     if not isinstance(method, MethodId):
         method = MethodId.parse(method)
-    if method.family == "cholqr" or method.orientation != "row":
-        raise ValueError("the distributed driver runs the row-oriented Gram-Schmidt schedule")
+    if method.family == "cholqr":
+        raise ValueError("the distributed driver runs the Gram-Schmidt methods")
+    # col and row orientation give bitwise-identical factors: both run the
+    # row-oriented step schedule here (as on one GPU)
     family, variant = method.family, method.variant
     m_loc, n = (int(s) for s in Z_local.shape)
     if n < 1 or op.dim != m_loc:

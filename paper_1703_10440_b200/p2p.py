@@ -94,7 +94,7 @@ class PeerGroup:
 def supported(op, method):
     from .distributed import DistCsrSpdOperator
 
-    return (isinstance(op, DistCsrSpdOperator) and op.local_apply is None and method.orientation == "row"
+    return (isinstance(op, DistCsrSpdOperator) and op.local_apply is None
             and method.variant in ("ha", "hp") and method.family in ("mgs", "cgs"))
 
 
