@@ -137,7 +137,10 @@ AQR_API aqr_status aqr_gs_factor_d2h(aqr_factor_args *args, double *Q_host, int6
 
 /* Host Z in, host Q / R out, with both transfers overlapped with the
  * factorization (row orientation): Z is copied in chunks of `chunk_cols`
- * columns (0 = n/8) on an internal stream; the step loop brings a chunk in
+ * columns (0 = ceil(n/8)) on an internal stream; when `ready` (page-locked
+ * host memory) is given, chunk c is copied only once *ready >= c + 1, so the
+ * caller can still be writing later chunks into Z_host (a GPU-side stream
+ * wait; the caller advances *ready in chunk order); the step loop brings a chunk in
  * when it needs it, after replaying the steps already done on it (the same
  * trailing passes and reduction trees: results are bitwise those of
  * aqr_gs_factor), and Q columns stream out as in aqr_gs_factor_d2h.  args->Q
@@ -146,7 +149,7 @@ AQR_API aqr_status aqr_gs_factor_d2h(aqr_factor_args *args, double *Q_host, int6
  * then runs aqr_gs_factor_d2h.  Returns after all copies completed. */
 AQR_API aqr_status aqr_gs_factor_pinned(aqr_factor_args *args, const double *Z_host, int64_t ldzh,
                                         double *Q_host, int64_t ldqh, double *R_host, int64_t ldrh,
-                                        int64_t chunk_cols, void *stream);
+                                        int64_t chunk_cols, const uint32_t *ready, void *stream);
 
 /* Same, with HOST Z/Q/R (column-major, ld = m / m / n) and a host-side
  * operator description (dense A, or CSR with int64 indptr/indices as the

@@ -93,6 +93,72 @@ _STAGE_THREADS = 8
 _pool = None
 
 
+class StagedHost:
+    """Page-locked column-major copy of a host matrix, filled concurrently.
+
+    ``a`` (numpy array or CPU tensor, m x n) is copied column by column on
+    the host thread pool, chunk after chunk (chunks of ``chunk`` columns);
+    ``ready`` (a page-locked uint32) counts the chunks that are complete, in
+    order, so the device can start copying chunk c once ready >= c + 1
+    (aqr_gs_factor_pinned) while later chunks are still being written.  A
+    tensor that already is page-locked, fp64 and column-major is used as it
+    is (``ready`` is None).
+    """
+
+    def __init__(self, a, chunk):
+        import threading
+
+        t = torch()
+        if is_torch(a) and a.is_pinned() and a.dtype == t.float64 and leading_dim(a) is not None:
+            self.T, self.ld, self.ready, self._futs = a, leading_dim(a), None, []
+            return
+        global _pool
+        if _pool is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="aqr-h2d")
+        m, n = a.shape
+        self.stage = t.empty((n, m), dtype=t.float64, pin_memory=True)
+        self.T, self.ld = self.stage.t(), max(m, 1)
+        self.flag = t.zeros(1, dtype=t.int32, pin_memory=True)
+        self.ready = self.flag.data_ptr()
+        flag = self.flag.numpy()
+        if is_torch(a):
+            src, dst = a.t(), self.stage
+            copy = lambda j: dst[j].copy_(src[j])  # noqa: E731
+        else:
+            src, dst = np.asarray(a, dtype=np.float64).T, self.stage.numpy()
+            copy = lambda j: np.copyto(dst[j], src[j])  # noqa: E731
+        w = max(1, int(chunk))
+        nch = (n + w - 1) // w
+        left = [min(w, n - c * w) for c in range(nch)]
+        state = {"next": 0, "error": None}
+        lock = threading.Lock()
+
+        def task(c, j):
+            try:
+                copy(j)
+            except BaseException as exc:  # never leave the device waiting
+                state["error"] = exc
+            with lock:
+                left[c] -= 1
+                while state["next"] < nch and left[state["next"]] == 0:
+                    state["next"] += 1
+                if state["error"] is not None:
+                    state["next"] = nch
+                flag[0] = state["next"]
+
+        self._state = state
+        self._futs = [_pool.submit(task, c, j) for c in range(nch) for j in range(c * w, min(n, (c + 1) * w))]
+
+    def finish(self):
+        """Wait for the copy tasks; re-raise a copy error."""
+        for f in self._futs:
+            f.result()
+        if self._futs and self._state["error"] is not None:
+            raise self._state["error"]
+
+
 def to_pinned_f(a):
     """(page-locked column-major fp64 host tensor (m, n), ld) holding ``a``
     (numpy array or CPU tensor); ``a`` itself when it already is one."""

@@ -11,6 +11,7 @@
 // reductions in the last CTA, so there are no separate reduction launches.
 // The column form runs the same kernels one column at a time, so both
 // orientations return bitwise-identical Q, R.
+#include <cuda.h>  // driver types for cuStreamWaitValue32 (fetched at run time, no link)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +22,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/aqr_b200.h"
@@ -1129,8 +1131,24 @@ static void keep_pool_memory() {
     done.push_back(dev);
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point table (the
+// library does not link libcuda; nullptr when unavailable).
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValue32Fn wait_value32() {
+    static const WaitValue32Fn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (WaitValue32Fn) nullptr;
+        return (WaitValue32Fn)p;
+    }();
+    return fn;
+}
+
 aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_t ldzh, double *Q_host,
-                                int64_t ldqh, double *R_host, int64_t ldrh, int64_t chunk_cols, void *stream) {
+                                int64_t ldqh, double *R_host, int64_t ldrh, int64_t chunk_cols,
+                                const uint32_t *ready, void *stream) {
     if (!a || !Z_host || !Q_host || !R_host) return set_err(AQR_EARG, "null args / host buffers");
     const int64_t m = a->m, n = a->n;
     if (n < 1 || m < n) return set_err(AQR_EDIM, "need m >= n >= 1");
@@ -1142,11 +1160,27 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
     // with a user operator, whose apply_block must see all n columns in one
     // call (gram_schmidt.py:136; the pipeline applies it chunk by chunk).
     const bool hp_callback = a->variant == AQR_HP && a->op && a->op->kind == AQR_OP_CALLBACK;
+    const int64_t w = chunk_cols > 0 ? chunk_cols : std::max<int64_t>(1, (n + 7) / 8);
+    const int64_t nchunks = (n + w - 1) / w;
+    // host-side wait for the staging producer (when the stream wait is unavailable)
+    auto host_wait = [&](uint32_t v) {
+        if (!ready) return;
+        while (*(const volatile uint32_t *)ready < v) std::this_thread::yield();
+    };
     if ((a->orientation != AQR_ROW && col_schedule_mode() != 0) || hp_callback) {
+        host_wait((uint32_t)nchunks);
         AQR_CUDA(copy_cols(a->Q, a->ldq, Z_host, ldzh, m, n, cudaMemcpyHostToDevice, s));
         return aqr_gs_factor_d2h(a, Q_host, ldqh, R_host, ldrh, stream);
     }
-    const int64_t w = chunk_cols > 0 ? chunk_cols : std::max<int64_t>(1, (n + 7) / 8);
+    CUdeviceptr ready_dev = 0;
+    WaitValue32Fn wfn = ready ? wait_value32() : nullptr;
+    if (wfn) {
+        void *dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, const_cast<uint32_t *>(ready), 0) == cudaSuccess)
+            ready_dev = (CUdeviceptr)dp;
+        else
+            wfn = nullptr;
+    }
     Pipe pp;
     for (int64_t c0 = 0; c0 < n; c0 += w) pp.bounds.push_back(c0);
     pp.bounds.push_back(n);
@@ -1169,6 +1203,16 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
             break;
         }
         pp.ev.push_back(e);
+        if (ready) {  // chunk c is in host memory once *ready >= c + 1 (staged by the caller)
+            if (wfn) {
+                if (wfn((CUstream)h2d.side, ready_dev, (cuuint32_t)(c + 1), CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+                    st = set_err(AQR_ECUDA, "cuStreamWaitValue32");
+                    break;
+                }
+            } else {
+                host_wait((uint32_t)(c + 1));
+            }
+        }
         if (copy_cols(a->Q + c0 * a->ldq, a->ldq, Z_host + c0 * ldzh, ldzh, m, cw, cudaMemcpyHostToDevice,
                       h2d.side) != cudaSuccess ||
             cudaEventRecord(e, h2d.side) != cudaSuccess)

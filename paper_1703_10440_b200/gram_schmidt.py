@@ -189,7 +189,9 @@ def _gs_factor(Z, op, family, variant, orientation):
 
     host_in = not (D.is_torch(Z) and Z.is_cuda)
     if host_in:  # Z stays on the host; aqr_gs_factor_pinned streams it in
-        Zh, ldzh = D.to_pinned_f(Z)
+        chunk = _chunk_cols() or max(1, (n + 7) // 8)
+        staged = D.StagedHost(Z, chunk)  # page-locked copy, filled while the device starts
+        Zh, ldzh = staged.T, staged.ld
         Q = D.empty_f(m, n)
         Zd, ldz = Q, m
     else:
@@ -222,7 +224,8 @@ def _gs_factor(Z, op, family, variant, orientation):
         Qh = t.empty((n, m), dtype=t.float64, pin_memory=True).t()
         Rh = t.empty((n, n), dtype=t.float64, pin_memory=True).t()
         status = L.aqr_gs_factor_pinned(ctypes.byref(a), Zh.data_ptr(), ldzh, Qh.data_ptr(), m, Rh.data_ptr(), n,
-                                        _chunk_cols(), D.stream_ptr())
+                                        chunk, staged.ready, D.stream_ptr())
+        staged.finish()
         if D.is_torch(Z):
             back = lambda T: Qh if T is Q else Rh  # noqa: E731
         else:
