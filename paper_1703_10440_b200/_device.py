@@ -159,42 +159,6 @@ class StagedHost:
             raise self._state["error"]
 
 
-def to_pinned_f(a):
-    """(page-locked column-major fp64 host tensor (m, n), ld) holding ``a``
-    (numpy array or CPU tensor); ``a`` itself when it already is one."""
-    t = torch()
-    if is_torch(a):
-        if a.is_pinned() and a.dtype == t.float64 and leading_dim(a) is not None:
-            return a, leading_dim(a)
-        m, n = a.shape
-        stage = t.empty((n, m), dtype=t.float64, pin_memory=True)
-        stage.copy_(a.t())
-        return stage.t(), max(m, 1)
-    A = np.asarray(a, dtype=np.float64)
-    m, n = A.shape
-    stage = t.empty((n, m), dtype=t.float64, pin_memory=True)
-    _copy_threaded(stage.numpy(), A.T)
-    return stage.t(), max(m, 1)
-
-
-def _copy_threaded(dst, src):
-    """dst[:] = src for (n, m) arrays, row chunks on the host thread pool."""
-    global _pool
-    if _pool is None:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="aqr-h2d")
-    n = dst.shape[0]
-    if dst.nbytes < _STAGE_MIN_BYTES or n < 2:
-        np.copyto(dst, src)
-        return
-    nchunks = min(n, 4 * _STAGE_THREADS)
-    bounds = [(k * n) // nchunks for k in range(nchunks + 1)]
-    futs = [_pool.submit(np.copyto, dst[b0:b1], src[b0:b1]) for b0, b1 in zip(bounds[:-1], bounds[1:]) if b1 > b0]
-    for f in futs:
-        f.result()
-
-
 def _h2d_staged(A, dev):
     global _pool
     t = torch()
