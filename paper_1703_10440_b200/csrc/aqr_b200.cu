@@ -328,8 +328,13 @@ aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx
         return launched("dense_gemm_kernel");
     }
     dim3 grid((unsigned)((m + aqr::kG2BM - 1) / aqr::kG2BM), (unsigned)((k + aqr::kG2BN - 1) / aqr::kG2BN));
-    aqr::dense_gemm2_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
-    return launched("dense_gemm2_kernel");
+    if (gv == 2) {
+        aqr::dense_gemm2_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
+        return launched("dense_gemm2_kernel");
+    }
+    AQR_TRY(ensure_smem(aqr::dense_gemm3_kernel, aqr::kG3Smem));
+    aqr::dense_gemm3_kernel<<<grid, 256, aqr::kG3Smem, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
+    return launched("dense_gemm3_kernel");
 }
 
 aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,

@@ -1476,4 +1476,95 @@ __global__ void __launch_bounds__(256, 1)
         }
 }
 
+// Same tiles, operands streamed into a 3-stage shared-memory ring with
+// cp.async (no register staging: <= 128 registers, 2 CTAs per SM).
+constexpr int kG3Stages = 3;
+constexpr size_t kG3StageWords = (size_t)kG2BK * kG2BM + (size_t)kG2BK * kG2BN;
+constexpr size_t kG3Smem = kG3Stages * kG3StageWords * sizeof(double);
+__device__ __forceinline__ void cp_async8_g2s(double *dst, const double *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__global__ void __launch_bounds__(256, 2)
+    dense_gemm3_kernel(int64_t m, int64_t ncols, int64_t k, const double *__restrict__ A, int64_t lda,
+                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y, int64_t ldy) {
+    extern __shared__ __align__(16) double g3[];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int64_t i0 = (int64_t)blockIdx.x * kG2BM, c0 = (int64_t)blockIdx.y * kG2BN;
+    const int64_t nk = (ncols + kG2BK - 1) / kG2BK;
+    auto As = [&](int st) { return g3 + (size_t)st * kG3StageWords; };            // [BK][BM]
+    auto Xs = [&](int st) { return g3 + (size_t)st * kG3StageWords + kG2BK * kG2BM; };  // [BK][BN]
+    auto issue = [&](int64_t kt) {
+        if (kt < nk) {
+            const int st = (int)(kt % kG3Stages);
+            const int64_t j0 = kt * kG2BK;
+            double *as = As(st), *xs = Xs(st);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int ii = tid & 127, jj = (tid >> 7) + 2 * u;
+                const int64_t gi = i0 + ii, gj = j0 + jj;
+                if (gi < m && gj < ncols) cp_async8_g2s(as + jj * kG2BM + ii, A + gi + gj * lda);
+                else as[jj * kG2BM + ii] = 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int jj = tid & 15, cc = (tid >> 4) + 16 * u;
+                const int64_t gj = j0 + jj, gc = c0 + cc;
+                if (gj < ncols && gc < k) cp_async8_g2s(xs + jj * kG2BN + cc, X + gj + gc * ldx);
+                else xs[jj * kG2BN + cc] = 0.0;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+#pragma unroll
+    for (int s = 0; s < kG3Stages - 1; ++s) issue(s);
+    for (int64_t kt = 0; kt < nk; ++kt) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kG3Stages - 2) : "memory");
+        __syncthreads();  // tile kt landed; tile kt-1's stage is free for kt+2
+        issue(kt + kG3Stages - 1);
+        const int st = (int)(kt % kG3Stages);
+        const double *as = As(st), *xs = Xs(st);
+        const int kmax = (ncols - kt * kG2BK) < kG2BK ? (int)(ncols - kt * kG2BK) : kG2BK;
+        if (kmax == kG2BK) {
+#pragma unroll
+            for (int jj = 0; jj < kG2BK; ++jj) {
+                double av[8], xv[4];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) av[a] = as[jj * kG2BM + ty + 16 * a];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) xv[b] = xs[jj * kG2BN + tx + 16 * b];
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(av[a], xv[b]));
+            }
+        } else {
+            for (int jj = 0; jj < kmax; ++jj) {
+                double av[8], xv[4];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) av[a] = as[jj * kG2BM + ty + 16 * a];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) xv[b] = xs[jj * kG2BN + tx + 16 * b];
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(av[a], xv[b]));
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int64_t gi = i0 + ty + 16 * a, gc = c0 + tx + 16 * b;
+            if (gi < m && gc < k) Y[gi + gc * ldy] = acc[a][b];
+        }
+}
+
 }  // namespace aqr
