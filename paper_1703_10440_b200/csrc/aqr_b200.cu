@@ -288,6 +288,11 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         return launched("csr_step_kernel");
     }
     const int32_t mr = op->max_row_nnz;
+    if (k > 1 && (mr > 8 || mr <= 0)) {  // long (or unknown) rows: CTA = (8 columns, 256 rows)
+        const int64_t nb = (op->m + aqr::kBlock - 1) / aqr::kBlock;
+        aqr::csr_spmm2_kernel<4, 8, 2><<<(unsigned)(((k + 7) / 8) * nb), aqr::kBlock, 0, s>>>(a);
+        return launched("csr_spmm2_kernel");
+    }
     if (mr >= 1 && mr <= 4)
         aqr::csr_row_kernel<4><<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
     else if (mr == 5)

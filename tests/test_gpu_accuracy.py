@@ -187,3 +187,15 @@ def test_ragged_m_large_tiles_against_oracle(aqr):
         tq, tr = parity.tolerance(Z, ("csr", ip, ix, dv), meth)
         eq, er = parity.factor_errors(r.Q, r.R, o.Q, o.R)
         assert eq <= tq and er <= tr, (meth, eq, tq, er, tr)
+
+
+def test_long_row_block_apply_bitwise(aqr):
+    """SpMM for rows longer than every row batch (csr_spmm2_kernel): each
+    output column bitwise the reference's csr_matvec (_kernels_impl.py:50-56)."""
+    ip, ix, dv = _ragged_spd_csr(2000, 11)
+    X = np.asfortranarray(np.random.default_rng(12).standard_normal((2000, 13)))
+    for hint in (None, 0):
+        op = aqr.CsrSpdOperator(ip, ix, dv, max_row_nnz=hint)
+        Y = op.apply_block(X)
+        for c in range(X.shape[1]):
+            assert np.array_equal(Y[:, c], O.csr_matvec(ip, ix, dv, X[:, c])), (hint, c)
