@@ -652,6 +652,36 @@ struct HostOut {
     cudaEvent_t ev = nullptr;
 };
 
+int catchup_mode() {  // AQR_CATCHUP=0: one trailing launch (+ totals) per caught-up step (A/B)
+    static const int v = [] {
+        const char *e = std::getenv("AQR_CATCHUP");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+template <int RPT, bool HP, bool CGS>
+aqr_status launch_catchup_t(const aqr::CatchArgs &c, cudaStream_t s) {
+    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(c.w, 1);
+    AQR_TRY(ensure_smem(aqr::catchup_kernel<RPT, HP, CGS>, smem));
+    int o = 0;
+    AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, aqr::catchup_kernel<RPT, HP, CGS>, aqr::kBlock, smem));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c.ntiles, (int64_t)sm_count() * std::max(1, o)));
+    aqr::CatchArgs cc = c;
+    void *args[] = {&cc};
+    AQR_CUDA(cudaLaunchCooperativeKernel((const void *)aqr::catchup_kernel<RPT, HP, CGS>, grid, aqr::kBlock, args, smem, s));
+    return launched("catchup_kernel");
+}
+
+aqr_status launch_catchup(const aqr::CatchArgs &c, bool hp, bool cgs, cudaStream_t s) {
+    if (aqr::rows_per_thread(c.m) == 8) {
+        if (hp) return cgs ? launch_catchup_t<8, true, true>(c, s) : launch_catchup_t<8, true, false>(c, s);
+        return cgs ? launch_catchup_t<8, false, true>(c, s) : launch_catchup_t<8, false, false>(c, s);
+    }
+    if (hp) return cgs ? launch_catchup_t<1, true, true>(c, s) : launch_catchup_t<1, true, false>(c, s);
+    return cgs ? launch_catchup_t<1, false, true>(c, s) : launch_catchup_t<1, false, false>(c, s);
+}
+
 // Host-input pipeline (aqr_gs_factor_pinned): Z arrives in column chunks on
 // an H2D stream.  A chunk joins the live columns when the step loop needs
 // it, after a catch-up of the steps already done: the trailing passes
@@ -754,6 +784,32 @@ struct Run {
         if (hp) {  // X = op.apply_block(Zw), chunk by chunk
             AQR_TRY(op_apply(a->op, w, col(W, ldw, c0), ldw, col(X, m, c0), m, s));
             mv += w;
+        }
+        // steps 0 .. i-1 in one cooperative launch (HA / naive: HP's kernel
+        // needs 160 registers and was measured slower than per-step launches)
+        if (i > 0 && catchup_mode() != 0 && !hp) {
+            aqr::CatchArgs c;
+            std::memset(&c, 0, sizeof c);
+            c.m = m;
+            c.n = n;
+            c.ntiles = (int32_t)aqr::num_tiles(m);
+            c.c0 = (int32_t)c0;
+            c.w = (int32_t)w;
+            c.k1 = (int32_t)i;
+            c.W = W;
+            c.ldw = ldw;
+            c.X = X;
+            c.ldx = m;
+            c.Z0 = Z0;
+            c.ldz0 = m;
+            c.vall = pp->vall;
+            c.p_direct = (hp || naive) ? 1 : 0;
+            c.Rt = Rt;
+            c.partial = pp->partial2;
+            c.status = status;
+            AQR_TRY(launch_catchup(c, hp, cgs, s));
+            live = c1;
+            return AQR_OK;
         }
         for (int64_t k = 0; k < i; ++k) {
             aqr::TrailArgs t = trail(k, c0, c1);

@@ -29,6 +29,7 @@
 // (_kernels_impl.py:24-56) and are therefore bitwise equal to it.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -621,6 +622,117 @@ __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
     trail_body<RPT, CU, HP, CGS>(a, blockIdx.x, blockIdx.y, wsum);
     trace_mark(a.trace, 2);
     // totals: the next step's norm kernel (RrowIn) or rrow_reduce_kernel
+}
+
+// ---------------------------------------------------------------------------
+// Catch-up of a newly arrived chunk of columns (host-input pipeline): the
+// trailing passes of steps 0 .. k1-1 restricted to the chunk, in ONE
+// cooperative launch -- per step a pass over the (tile, column) units, a grid
+// barrier, the chunk's R-row totals (block_totals, CTA b: column b), a grid
+// barrier.  The chunk (w x m) stays in L2 across the steps; the launches and
+// drains of 2 k1 small kernels disappear.  Per unit the same chain and
+// trees as trail_body, totals as rrow_reduce_kernel: bitwise identical.
+// ---------------------------------------------------------------------------
+struct CatchArgs {
+    int64_t m, n;
+    int32_t ntiles, c0, w, k1;
+    double *W;
+    int64_t ldw;
+    double *X;  // HP
+    int64_t ldx;
+    const double *Z0;  // CGS
+    int64_t ldz0;
+    const double *vall;  // per-step vectors, ld m: HA x_k (p_k = x_k / r_kk), HP / naive p_k
+    int32_t p_direct;
+    double *Rt;       // n x n row-major
+    double *partial;  // [w][ntiles]
+    const int32_t *status;
+};
+
+template <int RPT, bool HP, bool CGS>
+__global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    if (failed(a.status)) return;  // uniform: set before this launch
+    extern __shared__ double wsum[];  // [kWarps][w]
+    __shared__ double tot1[1];
+    __shared__ double sm1[kWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = 0; k < a.k1; ++k) {
+        const bool upd = k > 0;
+        const double rii = a.p_direct ? 1.0 : __ldcg(a.Rt + (int64_t)k * a.n + k);
+        const double *qprev = upd ? a.W + (int64_t)(k - 1) * a.ldw : nullptr;
+        const double *psrc = a.vall + (int64_t)k * a.m;
+        const double *pprev = (HP && upd) ? a.vall + (int64_t)(k - 1) * a.m : nullptr;
+        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {  // unit = (tile, all w columns)
+            const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
+            double q[RPT], p[RPT], pp[RPT];
+            bool ok[RPT];
+#pragma unroll
+            for (int v = 0; v < RPT; ++v) {
+                const int64_t r = row0 + (int64_t)v * kBlock;
+                ok[v] = r < a.m;
+                q[v] = (ok[v] && upd) ? __ldcg(qprev + r) : 0.0;
+                const double ps = ok[v] ? __ldcg(psrc + r) : 0.0;
+                p[v] = a.p_direct ? ps : ps / rii;
+                pp[v] = (HP && ok[v] && upd) ? __ldcg(pprev + r) : 0.0;
+            }
+            for (int c0 = 0; c0 < a.w; c0 += 2) {
+                double z[2][RPT], x[2][RPT], acc[2];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int j = a.c0 + c0 + c;
+                    const bool cj = c0 + c < a.w;
+#pragma unroll
+                    for (int v = 0; v < RPT; ++v) {
+                        const int64_t r = row0 + (int64_t)v * kBlock;
+                        z[c][v] = (cj && ok[v]) ? __ldcg(a.W + (int64_t)j * a.ldw + r) : 0.0;
+                        if (HP) x[c][v] = (cj && ok[v] && upd) ? __ldcg(a.X + (int64_t)j * a.ldx + r) : 0.0;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int j = a.c0 + c0 + c;
+                    const bool cj = c0 + c < a.w;
+                    const double rj = (cj && upd) ? __ldcg(a.Rt + (int64_t)(k - 1) * a.n + j) : 0.0;
+                    acc[c] = 0.0;
+#pragma unroll
+                    for (int v = 0; v < RPT; ++v) {
+                        const int64_t r = row0 + (int64_t)v * kBlock;
+                        if (upd) {
+                            z[c][v] = __dsub_rn(z[c][v], __dmul_rn(rj, q[v]));
+                            if (cj && ok[v]) a.W[(int64_t)j * a.ldw + r] = z[c][v];
+                            if (HP) {
+                                x[c][v] = __dsub_rn(x[c][v], __dmul_rn(rj, pp[v]));
+                                if (cj && ok[v]) a.X[(int64_t)j * a.ldx + r] = x[c][v];
+                            }
+                        }
+                        const double d = CGS ? ((cj && ok[v]) ? __ldcg(a.Z0 + (int64_t)j * a.ldz0 + r) : 0.0) : z[c][v];
+                        acc[c] = fma(p[v], d, acc[c]);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double sw = warp_sum(acc[c]);
+                    if (lane == 0 && c0 + c < a.w) wsum[warp * a.w + c0 + c] = sw;
+                }
+            }
+            __syncthreads();
+            for (int c = threadIdx.x; c < a.w; c += kBlock) {
+                double s = wsum[c];
+#pragma unroll
+                for (int w2 = 1; w2 < kWarps; ++w2) s = __dadd_rn(s, wsum[w2 * a.w + c]);
+                a.partial[(int64_t)c * a.ntiles + tile] = s;
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        for (int cc = blockIdx.x; cc < a.w; cc += gridDim.x) {
+            block_totals<1>(a.partial + (int64_t)cc * a.ntiles, a.ntiles, a.ntiles, tot1, sm1, SyncAll());
+            if (threadIdx.x == 0) a.Rt[(int64_t)k * a.n + a.c0 + cc] = tot1[0];
+        }
+        grid.sync();
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -5,8 +5,9 @@ The knobs are read once per process (include/aqr_b200.h, DESIGN.md section
 bitwise with the default build's: the TMA-bulk trailing kernel (with and
 without the L2 hint), the unpipelined SpMV step, the separate R-row
 reduction launch, launches without programmatic dependent launch, the
-materialized copy of Z, and the column-oriented loop for the col methods
-(by default they run the row-oriented step schedule).
+materialized copy of Z, the column-oriented loop for the col methods
+(by default they run the row-oriented step schedule), and the per-step
+catch-up launches of the host-input pipeline.
 """
 
 import os
@@ -36,6 +37,13 @@ for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "cgs-hp-row", "mgs-naive-
     r = aqr.factorize(Zd, op, meth)
     out[meth + "|Q"] = r.Q.cpu().numpy()
     out[meth + "|R"] = r.R.cpu().numpy()
+import os
+os.environ["AQR_CHUNK_COLS"] = "3"  # host input: the chunked pipeline and its catch-up
+Zn = np.asfortranarray(Z)
+for meth in ("mgs-ha-row", "cgs-ha-row", "mgs-hp-row", "mgs-naive-col"):
+    r = aqr.factorize(Zn, op, meth)
+    out[meth + "|Qh"] = r.Q
+    out[meth + "|Rh"] = r.R
 np.savez({path!r}, **out)
 """
 
@@ -62,6 +70,7 @@ def default_factors(tmp_path_factory):
     {"AQR_PDL": "0"},
     {"AQR_DIRECT": "0"},
     {"AQR_COL_SCHEDULE": "1"},
+    {"AQR_CATCHUP": "0"},
 ])
 def test_variant_bitwise_equal_default(default_factors, knobs, tmp_path):
     got = _run(knobs, tmp_path / "variant.npz")
