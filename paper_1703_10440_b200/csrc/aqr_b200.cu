@@ -785,9 +785,8 @@ struct Run {
             AQR_TRY(op_apply(a->op, w, col(W, ldw, c0), ldw, col(X, m, c0), m, s));
             mv += w;
         }
-        // steps 0 .. i-1 in one cooperative launch (HA / naive: HP's kernel
-        // needs 160 registers and was measured slower than per-step launches)
-        if (i > 0 && catchup_mode() != 0 && !hp) {
+        // steps 0 .. i-1 in one cooperative launch
+        if (i > 0 && catchup_mode() != 0) {
             aqr::CatchArgs c;
             std::memset(&c, 0, sizeof c);
             c.m = m;

@@ -677,10 +677,11 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
                 p[v] = a.p_direct ? ps : ps / rii;
                 pp[v] = (HP && ok[v] && upd) ? __ldcg(pprev + r) : 0.0;
             }
-            for (int c0 = 0; c0 < a.w; c0 += 2) {
-                double z[2][RPT], x[2][RPT], acc[2];
+            constexpr int CU = HP ? 1 : 2;  // HP carries x too: one column per iteration (registers)
+            for (int c0 = 0; c0 < a.w; c0 += CU) {
+                double z[CU][RPT], x[CU][RPT], acc[CU];
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
+                for (int c = 0; c < CU; ++c) {
                     const int j = a.c0 + c0 + c;
                     const bool cj = c0 + c < a.w;
 #pragma unroll
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
+                for (int c = 0; c < CU; ++c) {
                     const int j = a.c0 + c0 + c;
                     const bool cj = c0 + c < a.w;
                     const double rj = (cj && upd) ? __ldcg(a.Rt + (int64_t)(k - 1) * a.n + j) : 0.0;
@@ -712,7 +713,7 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
                     }
                 }
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
+                for (int c = 0; c < CU; ++c) {
                     const double sw = warp_sum(acc[c]);
                     if (lane == 0 && c0 + c < a.w) wsum[warp * a.w + c0 + c] = sw;
                 }
