@@ -210,8 +210,9 @@ def run_b200(args, rank, world, local_rank):
         fn = lambda Z_, op_, o_: aqr.cgs(Z_, op_, variant, o_)  # noqa: E731
     stream = torch.cuda.current_stream()
 
-    for _ in range(args.warmup):
-        fn(Zd, op, orientation)
+    res = None
+    for _ in range(args.warmup):  # as in the timed loop, the previous result stays alive
+        res = fn(Zd, op, orientation)  # during the next call (two cached Q blocks)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region (value) ----
