@@ -273,15 +273,15 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         if (sv == 3)
             launch_pdl(aqr::csr_step_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
         else if (mr >= 1 && mr <= 4)
-            launch_pdl(aqr::csr_step_pf_kernel<4, 3>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_pf_kernel<4, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
         else if (mr == 5)
-            launch_pdl(aqr::csr_step_pf_kernel<5, 3>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_pf_kernel<5, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
         else if (mr == 6)
-            launch_pdl(aqr::csr_step_pf_kernel<6, 3>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_pf_kernel<6, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
         else if (mr == 7)
-            launch_pdl(aqr::csr_step_pf_kernel<7, 3>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_pf_kernel<7, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
         else if (mr == 8)
-            launch_pdl(aqr::csr_step_pf_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
+            launch_pdl(aqr::csr_step_pf_kernel<8, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
         else  // long or unknown rows: batches of 8 without the row look-ahead
             launch_pdl(aqr::csr_step_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
         timer_end(tix, s);

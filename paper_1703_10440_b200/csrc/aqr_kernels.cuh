@@ -55,6 +55,9 @@ __host__ __device__ inline int64_t num_tiles(int64_t m) {
 // b.  Totals are block_totals over the G partials.  G is one wave of the
 // kernel that forms the partials: 3 CTAs/SM for the software-pipelined
 // fused SpMV step (HA / naive), 4 CTAs/SM for the HP column update.
+#ifndef AQR_SPMV_MINB
+#define AQR_SPMV_MINB 3  // resident fused-SpMV CTAs per SM (the HA norm grid is this x 148)
+#endif
 #ifndef AQR_NORM_GRID_HA
 #define AQR_NORM_GRID_HA (148 * 3)
 #endif
