@@ -1295,8 +1295,12 @@ __device__ __forceinline__ void load_entries(const CsrArgs &a, int s, int e, int
     }
 }
 
-template <int B>
-__device__ __forceinline__ void csr_step_body_pf(const CsrArgs &a, int64_t cta, int64_t G) {
+// PRE: the first rows' pointers and entries (the operator is read-only for
+// the whole factorization) are loaded before the grid-dependency wait, so
+// their two dependent round trips overlap the tail of the previous kernel;
+// returns false when an earlier step failed.
+template <int B, bool PRE = false>
+__device__ __forceinline__ bool csr_step_body_pf(const CsrArgs &a, int64_t cta, int64_t G) {
     const bool upd = a.r != nullptr;
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t stride = G * kBlock;
@@ -1310,6 +1314,10 @@ __device__ __forceinline__ void csr_step_body_pf(const CsrArgs &a, int64_t cta, 
     int c[B];
     double v[B];
     load_entries<B>(a, s, e, c, v);
+    if (PRE) {
+        pdl_wait();
+        if (failed(a.out.status)) return false;
+    }
     const double rj = a.rin.partial ? rrow_first(a.rin, cta == 0) : (upd ? *a.r : 0.0);
     for (int64_t blk = cta; blk < nblk; blk += G) {
         // stage 1: pointers two rows ahead; stage 2: entries one row ahead
@@ -1359,15 +1367,22 @@ __device__ __forceinline__ void csr_step_body_pf(const CsrArgs &a, int64_t cta, 
     pdl_trigger();
     norm_cta_partial(a.out, t, zz, xx, cta);
     norm_last_cta(a.out, (unsigned)G);
+    return true;
 }
 
+// AQR_SPMV_PREWAIT=0: wait before any load (A/B; config 2 HA 7.60 vs 7.62 ms).
+#ifndef AQR_SPMV_PREWAIT
+#define AQR_SPMV_PREWAIT 1
+#endif
 template <int B, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) csr_step_pf_kernel(CsrArgs a) {
     trace_mark(a.trace, 0);
-    pdl_wait();
-    trace_mark(a.trace, 1);
-    if (failed(a.out.status)) return;
-    csr_step_body_pf<B>(a, blockIdx.x, gridDim.x);
+    if (!AQR_SPMV_PREWAIT) {
+        pdl_wait();
+        if (failed(a.out.status)) return;
+    }
+    trace_mark(a.trace, 1);  // with PRE: before the wait
+    if (!csr_step_body_pf<B, AQR_SPMV_PREWAIT != 0>(a, blockIdx.x, gridDim.x)) return;
     rrow_rest(a.rin, blockIdx.x, gridDim.x);
     trace_mark(a.trace, 2);
 }
