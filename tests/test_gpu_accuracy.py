@@ -199,3 +199,70 @@ def test_long_row_block_apply_bitwise(aqr):
         Y = op.apply_block(X)
         for c in range(X.shape[1]):
             assert np.array_equal(Y[:, c], O.csr_matvec(ip, ix, dv, X[:, c])), (hint, c)
+
+
+EDGE_METHODS = [f"{f}-{v}-{o}" for f in ("mgs", "cgs") for v in ("naive", "ha", "hp") for o in ("col", "row")]
+
+
+def _tridiag_csr(m):
+    """1-D Laplacian + I (diag 3, off -1), sorted columns."""
+    rows, cols, vals = [], [], []
+    for i in range(m):
+        for j, v in ((i - 1, -1.0), (i, 3.0), (i + 1, -1.0)):
+            if 0 <= j < m:
+                rows.append(i), cols.append(j), vals.append(v)
+    from paper_1703_10440_b200 import csr_from_coo
+
+    op = csr_from_coo(m, np.array(rows), np.array(cols), np.array(vals))
+    return op.indptr, op.indices, op.data
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 1), (2, 2), (7, 7), (255, 3), (256, 1), (257, 5),
+                                 (300, 300), (1025, 17), (2049, 2)])
+def test_edge_shapes_all_methods_against_oracle(aqr, m, n):
+    """Single columns, square Z, m at and around the 256-row block and the
+    tile sizes, for all 12 methods with a dense and a CSR operator."""
+    rng = np.random.default_rng(np.random.SeedSequence([1703, 10440, 91, m, n]))
+    B = rng.standard_normal((m, m))
+    A = np.asfortranarray(B @ B.T / m + np.eye(m))
+    Z = np.asfortranarray(rng.standard_normal((m, n)))
+    ip, ix, dv = _tridiag_csr(m)
+    import torch
+
+    Zd = torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().t()
+    for spec, op in ((("dense", A), aqr.DenseSpdOperator(A)), (("csr", ip, ix, dv), aqr.CsrSpdOperator(ip, ix, dv))):
+        for meth in EDGE_METHODS:
+            r = aqr.factorize(Z, op, meth)
+            o = O.gs_factor(Z, spec, meth)
+            tq, tr = parity.tolerance(Z, spec, meth)
+            eq, er = parity.factor_errors(r.Q, r.R, o.Q, o.R)
+            assert eq <= tq and er <= tr, (spec[0], meth, eq, tq, er, tr)
+            assert np.array_equal(np.tril(r.R, -1), np.zeros((n, n)))
+            assert r.flagged_columns == o.flagged_columns, (spec[0], meth)
+            rd = aqr.factorize(Zd, op, meth)  # device input: bitwise the host-input pipeline
+            assert np.array_equal(rd.Q.cpu().numpy(), r.Q) and np.array_equal(rd.R.cpu().numpy(), r.R)
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_non_finite_input_breaks_down_like_the_oracle(aqr, bad):
+    """A non-finite entry in column 4 makes z'Az non-finite there: the same
+    BreakdownError column as the oracle (gram_schmidt.py:153-154), with a
+    non-finite value, for all 12 methods, host and device input."""
+    import math
+
+    import torch
+
+    m, n = 600, 7
+    rng = np.random.default_rng(np.random.SeedSequence([1703, 10440, 92]))
+    B = rng.standard_normal((m, m))
+    A = np.asfortranarray(B @ B.T / m + np.eye(m))
+    Z = np.asfortranarray(rng.standard_normal((m, n)))
+    Z[123, 4] = bad
+    for meth in EDGE_METHODS:
+        with pytest.raises(O.OracleBreakdown) as oinfo:
+            O.gs_factor(Z, ("dense", A), meth)
+        for Zin in (Z, torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().t()):
+            with pytest.raises(aqr.BreakdownError) as info:
+                aqr.factorize(Zin, aqr.DenseSpdOperator(A), meth)
+            assert info.value.column == oinfo.value.column == 4, meth
+            assert not math.isfinite(info.value.value), meth
