@@ -1513,8 +1513,8 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
                       : launch_p2p_trailing<false, false>(t, P, i, Rt + i * n + i, status, s);
         AQR_TRY(st);
         if (i + 1 < n) {
-            aqr::p2p_rrow_kernel<<<(unsigned)(n - 1 - i), aqr::kBlock, 0, s>>>(partial, ntiles, i + 1, P, i,
-                                                                          counters + 1, status);
+            launch_pdl(aqr::p2p_rrow_kernel, (unsigned)(n - 1 - i), aqr::kBlock, 0, s, (const double *)partial,
+                       (int32_t)ntiles, (int64_t)(i + 1), P, (int64_t)i, counters + 1, (const int32_t *)status);
             AQR_TRY(launched("p2p_rrow_kernel"));
         }
     }

@@ -165,8 +165,6 @@ __device__ __forceinline__ double p2p_xe(const CsrArgs &a, const P2PArgs &p, int
 // chains as the single-GPU kernels.
 template <int B>
 __global__ void __launch_bounds__(kBlock, 3) p2p_csr_step_kernel(CsrArgs a, P2PArgs p, int64_t i, double *Rt) {
-    pdl_wait();
-    if (failed(a.out.status)) return;
     const bool upd = i > 0;
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x, stride = G * kBlock;
@@ -179,7 +177,9 @@ __global__ void __launch_bounds__(kBlock, 3) p2p_csr_step_kernel(CsrArgs a, P2PA
     int ne = nrow < a.m ? __ldg(a.indptr + nrow + 1) : 0;
     int c[B];
     double v[B];
-    load_entries<B>(a, s, e, c, v);
+    load_entries<B>(a, s, e, c, v);  // the operator is read-only: before the wait
+    pdl_wait();
+    if (failed(a.out.status)) return;
     const double rj = p2p_rrow_in(p, i, Rt);
     for (int64_t blk = blockIdx.x; blk < nblk; blk += G) {
         const int64_t n2 = nrow + stride;
@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kBlock, 3) p2p_csr_step_kernel(CsrArgs a, P2PA
             v[h] = nv[h];
         }
     }
+    pdl_trigger();
     norm_cta_partial(a.out, t, zz, xx, blockIdx.x);
     p2p_norm_out(p, a.out, gridDim.x, i);
 }
@@ -300,6 +301,8 @@ __global__ void __launch_bounds__(kBlock) p2p_trailing_kernel(TrailArgs a, P2PAr
 __global__ void __launch_bounds__(kBlock) p2p_rrow_kernel(const double *partial, int32_t ntiles, int64_t jbeg,
                                                           P2PArgs p, int64_t i, unsigned *counter,
                                                           const int32_t *status) {
+    pdl_wait();
+    pdl_trigger();  // the next step's SpMV may launch (it waits for this grid)
     if (failed(status)) return;
     __shared__ double tot[1];
     __shared__ double sm[kWarps];
