@@ -151,6 +151,13 @@ AQR_API aqr_status aqr_gs_factor_pinned(aqr_factor_args *args, const double *Z_h
                                         double *Q_host, int64_t ldqh, double *R_host, int64_t ldrh,
                                         int64_t chunk_cols, const uint32_t *ready, void *stream);
 
+/* Column chunks the host-input pipeline uses for n columns (chunk_cols as
+ * passed to aqr_gs_factor_pinned; 0 = the library's schedule): writes the
+ * chunk boundaries (first 0, last n; at most max_bounds entries) and returns
+ * the number of chunks.  A caller staging Z for the `ready` counter fills
+ * chunk c = columns [bounds[c], bounds[c + 1]) in order. */
+AQR_API int64_t aqr_pipe_chunks(int64_t n, int64_t chunk_cols, int64_t *bounds, int64_t max_bounds);
+
 /* Same, with HOST Z/Q/R (column-major, ld = m / m / n) and a host-side
  * operator description (dense A, or CSR with int64 indptr/indices as the
  * reference's CsrSpdOperator holds them, operators.py:100-101).  Owns all

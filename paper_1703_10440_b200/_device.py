@@ -97,7 +97,8 @@ class StagedHost:
     """Page-locked column-major copy of a host matrix, filled concurrently.
 
     ``a`` (numpy array or CPU tensor, m x n) is copied column by column on
-    the host thread pool, chunk after chunk (chunks of ``chunk`` columns);
+    the host thread pool, chunk after chunk (chunk c = columns
+    ``bounds[c] .. bounds[c + 1] - 1``, the pipeline's schedule);
     ``ready`` (a page-locked uint32) counts the chunks that are complete, in
     order, so the device can start copying chunk c once ready >= c + 1
     (aqr_gs_factor_pinned) while later chunks are still being written.  A
@@ -105,7 +106,7 @@ class StagedHost:
     is (``ready`` is None).
     """
 
-    def __init__(self, a, chunk):
+    def __init__(self, a, bounds):
         import threading
 
         t = torch()
@@ -129,9 +130,9 @@ class StagedHost:
         else:
             src, dst = np.asarray(a, dtype=np.float64).T, self.stage.numpy()
             copy = lambda j: np.copyto(dst[j], src[j])  # noqa: E731
-        w = max(1, int(chunk))
-        nch = (n + w - 1) // w
-        left = [min(w, n - c * w) for c in range(nch)]
+        bounds = [int(b) for b in bounds]
+        nch = len(bounds) - 1
+        left = [bounds[c + 1] - bounds[c] for c in range(nch)]
         state = {"next": 0, "error": None}
         lock = threading.Lock()
 
@@ -149,7 +150,7 @@ class StagedHost:
                 flag[0] = state["next"]
 
         self._state = state
-        self._futs = [_pool.submit(task, c, j) for c in range(nch) for j in range(c * w, min(n, (c + 1) * w))]
+        self._futs = [_pool.submit(task, c, j) for c in range(nch) for j in range(bounds[c], bounds[c + 1])]
 
     def finish(self):
         """Wait for the copy tasks; re-raise a copy error."""

@@ -84,6 +84,7 @@ SIGNATURES = {
     "aqr_gs_factor_d2h": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_gs_factor_pinned": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                      c_i64, c_vp, c_vp]),
+    "aqr_pipe_chunks": (c_i64, [c_i64, c_i64, c_vp, c_i64]),
     "aqr_gs_factor_host": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32,
                                    c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64),
                                    ctypes.POINTER(c_dbl), c_vp, ctypes.POINTER(c_i64)]),

@@ -187,6 +187,15 @@ int pdl_mode() {
     return v;
 }
 
+// AQR_LDG_REVERSE=0: the LDG trailing kernel always walks forwards (A/B).
+int ldg_reverse_mode() {
+    static const int v = [] {
+        const char *e = std::getenv("AQR_LDG_REVERSE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                 Args... args) {
@@ -483,6 +492,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
         else    { if (cgs) TMA_LAUNCH(false, true); else TMA_LAUNCH(false, false); }
 #undef TMA_LAUNCH
     } else {
+        if (ldg_reverse_mode() == 0) a.reverse = 0;
         dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
         const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
 #define LAUNCH(RPT, CU, HP, CGS)                                                   \
@@ -662,11 +672,13 @@ int catchup_mode() {  // AQR_CATCHUP=0: one trailing launch (+ totals) per caugh
 
 template <int RPT, bool HP, bool CGS>
 aqr_status launch_catchup_t(const aqr::CatchArgs &c, cudaStream_t s) {
-    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(c.w, 1);
+    constexpr int kCu = HP ? 1 : 2;  // columns per unit (catchup_kernel)
+    const size_t smem = sizeof(double) * aqr::kWarps * kCu;
     AQR_TRY(ensure_smem(aqr::catchup_kernel<RPT, HP, CGS>, smem));
     int o = 0;
     AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, aqr::catchup_kernel<RPT, HP, CGS>, aqr::kBlock, smem));
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(c.ntiles, (int64_t)sm_count() * std::max(1, o)));
+    const int64_t units = (int64_t)c.ntiles * ((c.w + kCu - 1) / kCu);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)sm_count() * std::max(1, o)));
     aqr::CatchArgs cc = c;
     void *args[] = {&cc};
     AQR_CUDA(cudaLaunchCooperativeKernel((const void *)aqr::catchup_kernel<RPT, HP, CGS>, grid, aqr::kBlock, args, smem, s));
@@ -806,6 +818,7 @@ struct Run {
             c.Rt = Rt;
             c.partial = pp->partial2;
             c.status = status;
+            c.trace = trace_slot();
             AQR_TRY(launch_catchup(c, hp, cgs, s));
             live = c1;
             return AQR_OK;
@@ -1196,6 +1209,33 @@ static void keep_pool_memory() {
     done.push_back(dev);
 }
 
+// Column chunks of the host-input pipeline: chunk_cols > 0 gives uniform
+// chunks; 0 the default schedule (AQR_PIPE_SCHED: 0 uniform n/8, 1 n/8 then
+// halving towards the end, 2 also ramping up from n/32 at the start).  Small
+// chunks at the start let the first steps -- and the D2H of Q -- begin
+// earlier; small ones at the end shorten the tail after the last H2D
+// (catch-up of the last chunk, its steps and the D2H of its columns).
+int pipe_sched_mode() {
+    static const int v = [] {
+        const char *e = std::getenv("AQR_PIPE_SCHED");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+std::vector<int64_t> pipe_bounds(int64_t n, int64_t chunk_cols) {
+    std::vector<int64_t> b{0};
+    if (n <= 0) return b;
+    const int sched = chunk_cols > 0 ? 0 : pipe_sched_mode();
+    const int64_t w = chunk_cols > 0 ? chunk_cols : std::max<int64_t>(1, (n + 7) / 8);
+    int64_t c = 0;
+    if (sched == 2)  // ramp: w/4, w/2, then w
+        for (int64_t r = std::max<int64_t>(1, w / 4); r < w && c + r < n; r *= 2) b.push_back(c += r);
+    while (n - c > (sched >= 1 ? w : 0)) b.push_back(c = std::min(n, c + w));
+    while (c < n) b.push_back(c += std::max<int64_t>(1, (n - c) / 2));  // taper: halves, then 1
+    return b;
+}
+
 // cuStreamWaitValue32 through the runtime's driver entry point table (the
 // library does not link libcuda; nullptr when unavailable).
 typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -1209,6 +1249,12 @@ static WaitValue32Fn wait_value32() {
         return (WaitValue32Fn)p;
     }();
     return fn;
+}
+
+int64_t aqr_pipe_chunks(int64_t n, int64_t chunk_cols, int64_t *bounds, int64_t max_bounds) {
+    const std::vector<int64_t> b = pipe_bounds(n, chunk_cols);
+    for (size_t k = 0; k < b.size() && (int64_t)k < max_bounds; ++k) bounds[k] = b[k];
+    return (int64_t)b.size() - 1;
 }
 
 aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_t ldzh, double *Q_host,
@@ -1225,8 +1271,7 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
     // with a user operator, whose apply_block must see all n columns in one
     // call (gram_schmidt.py:136; the pipeline applies it chunk by chunk).
     const bool hp_callback = a->variant == AQR_HP && a->op && a->op->kind == AQR_OP_CALLBACK;
-    const int64_t w = chunk_cols > 0 ? chunk_cols : std::max<int64_t>(1, (n + 7) / 8);
-    const int64_t nchunks = (n + w - 1) / w;
+    const int64_t nchunks = (int64_t)pipe_bounds(n, chunk_cols).size() - 1;
     // host-side wait for the staging producer (when the stream wait is unavailable)
     auto host_wait = [&](uint32_t v) {
         if (!ready) return;
@@ -1247,8 +1292,7 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
             wfn = nullptr;
     }
     Pipe pp;
-    for (int64_t c0 = 0; c0 < n; c0 += w) pp.bounds.push_back(c0);
-    pp.bounds.push_back(n);
+    pp.bounds = pipe_bounds(n, chunk_cols);
     const size_t nch = pp.bounds.size() - 1;
     const int64_t ntiles = std::max<int64_t>(aqr::num_tiles(m), 1);
     keep_pool_memory();

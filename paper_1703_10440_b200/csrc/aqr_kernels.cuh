@@ -622,7 +622,13 @@ __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
     trace_mark(a.trace, 1);
     if (failed(a.status)) return;
     extern __shared__ double wsum[];  // [kWarps][cpg]
-    trail_body<RPT, CU, HP, CGS>(a, blockIdx.x, blockIdx.y, wsum);
+    // Odd steps walk the (tile, group) units backwards: CTAs are dispatched
+    // x-fastest, so the first units of this pass are the last ones the
+    // previous pass wrote -- still in L2.  Partials are per unit: bitwise
+    // independent of the walk.
+    const int tile = a.reverse ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+    const int group = a.reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
+    trail_body<RPT, CU, HP, CGS>(a, tile, group, wsum);
     trace_mark(a.trace, 2);
     // totals: the next step's norm kernel (RrowIn) or rrow_reduce_kernel
 }
@@ -650,14 +656,17 @@ struct CatchArgs {
     double *Rt;       // n x n row-major
     double *partial;  // [w][ntiles]
     const int32_t *status;
+    int32_t trace;    // AQR_TRACE builds: launch slot (-1 off)
 };
 
 template <int RPT, bool HP, bool CGS>
 __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
+    trace_mark(a.trace, 0);
+    trace_mark(a.trace, 1);
     if (failed(a.status)) return;  // uniform: set before this launch
-    extern __shared__ double wsum[];  // [kWarps][w]
+    extern __shared__ double wsum[];  // [kWarps][CU]
     __shared__ double tot1[1];
     __shared__ double sm1[kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -667,21 +676,32 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
         const double *qprev = upd ? a.W + (int64_t)(k - 1) * a.ldw : nullptr;
         const double *psrc = a.vall + (int64_t)k * a.m;
         const double *pprev = (HP && upd) ? a.vall + (int64_t)(k - 1) * a.m : nullptr;
-        for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {  // unit = (tile, all w columns)
+        // units (tile, CU columns), tile-major; CTA b walks the contiguous
+        // range [U b / G, U (b + 1) / G) (balanced to one unit) and reloads
+        // the step vectors only when the range enters a new tile
+        constexpr int CU = HP ? 1 : 2;  // HP carries x too: one column per unit (registers)
+        const int ng = (a.w + CU - 1) / CU;
+        const int64_t U = (int64_t)a.ntiles * ng;
+        const int64_t ub = U * blockIdx.x / gridDim.x, ue = U * (blockIdx.x + 1) / gridDim.x;
+        int cur = -1;
+        double q[RPT], p[RPT], pp[RPT];
+        bool ok[RPT];
+        for (int64_t u = ub; u < ue; ++u) {
+            const int tile = (int)(u / ng), c0 = (int)(u % ng) * CU;
             const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
-            double q[RPT], p[RPT], pp[RPT];
-            bool ok[RPT];
+            if (tile != cur) {
+                cur = tile;
 #pragma unroll
-            for (int v = 0; v < RPT; ++v) {
-                const int64_t r = row0 + (int64_t)v * kBlock;
-                ok[v] = r < a.m;
-                q[v] = (ok[v] && upd) ? __ldcg(qprev + r) : 0.0;
-                const double ps = ok[v] ? __ldcg(psrc + r) : 0.0;
-                p[v] = a.p_direct ? ps : ps / rii;
-                pp[v] = (HP && ok[v] && upd) ? __ldcg(pprev + r) : 0.0;
+                for (int v = 0; v < RPT; ++v) {
+                    const int64_t r = row0 + (int64_t)v * kBlock;
+                    ok[v] = r < a.m;
+                    q[v] = (ok[v] && upd) ? __ldcg(qprev + r) : 0.0;
+                    const double ps = ok[v] ? __ldcg(psrc + r) : 0.0;
+                    p[v] = a.p_direct ? ps : ps / rii;
+                    pp[v] = (HP && ok[v] && upd) ? __ldcg(pprev + r) : 0.0;
+                }
             }
-            constexpr int CU = HP ? 1 : 2;  // HP carries x too: one column per iteration (registers)
-            for (int c0 = 0; c0 < a.w; c0 += CU) {
+            {
                 double z[CU][RPT], x[CU][RPT], acc[CU];
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {
@@ -718,15 +738,16 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {
                     const double sw = warp_sum(acc[c]);
-                    if (lane == 0 && c0 + c < a.w) wsum[warp * a.w + c0 + c] = sw;
+                    if (lane == 0) wsum[warp * CU + c] = sw;
                 }
             }
             __syncthreads();
-            for (int c = threadIdx.x; c < a.w; c += kBlock) {
+            if (threadIdx.x < CU && c0 + (int)threadIdx.x < a.w) {
+                const int c = threadIdx.x;
                 double s = wsum[c];
 #pragma unroll
-                for (int w2 = 1; w2 < kWarps; ++w2) s = __dadd_rn(s, wsum[w2 * a.w + c]);
-                a.partial[(int64_t)c * a.ntiles + tile] = s;
+                for (int w2 = 1; w2 < kWarps; ++w2) s = __dadd_rn(s, wsum[w2 * CU + c]);
+                a.partial[(int64_t)(c0 + c) * a.ntiles + tile] = s;
             }
             __syncthreads();
         }
@@ -737,6 +758,7 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
         }
         grid.sync();
     }
+    trace_mark(a.trace, 2);
 }
 
 // ---------------------------------------------------------------------------

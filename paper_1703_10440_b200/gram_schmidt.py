@@ -176,7 +176,7 @@ def _expected_mv(variant, n, fail_col):
 def _chunk_cols():
     import os
 
-    return int(os.environ.get("AQR_CHUNK_COLS", "0"))  # 0: the library's default (n / 8)
+    return int(os.environ.get("AQR_CHUNK_COLS", "0"))  # 0: the library's schedule (aqr_pipe_chunks)
 
 
 def _gs_factor(Z, op, family, variant, orientation):
@@ -189,8 +189,10 @@ def _gs_factor(Z, op, family, variant, orientation):
 
     host_in = not (D.is_torch(Z) and Z.is_cuda)
     if host_in:  # Z stays on the host; aqr_gs_factor_pinned streams it in
-        chunk = _chunk_cols() or max(1, (n + 7) // 8)
-        staged = D.StagedHost(Z, chunk)  # page-locked copy, filled while the device starts
+        chunk = _chunk_cols()  # 0: the library's schedule
+        bounds = np.zeros(n + 1, dtype=np.int64)
+        nch = int(L.aqr_pipe_chunks(n, chunk, bounds.ctypes.data, n + 1))
+        staged = D.StagedHost(Z, bounds[: nch + 1])  # page-locked copy, filled while the device starts
         Zh, ldzh = staged.T, staged.ld
         Q = D.empty_f(m, n)
         Zd, ldz = Q, m

@@ -297,6 +297,32 @@ def test_pinned_host_input_streams_q_bitwise(aqr, meth, chunk, monkeypatch):
     assert rh.cost.mv_count == rd.cost.mv_count
 
 
+@pytest.mark.parametrize("sched", ["0", "1", "2"])
+def test_pipeline_chunk_schedules_bitwise(aqr, sched, monkeypatch):
+    """Every chunk schedule of the host-input pipeline (aqr_pipe_chunks:
+    uniform, tapered, ramped + tapered) -- catch-up launches over chunks of
+    1 .. n/8 columns, balanced (tile, column) unit ranges -- gives the
+    device-resident bits, for numpy (staged) and page-locked inputs."""
+    import torch
+
+    from paper_1703_10440_b200 import _lib, problems
+
+    monkeypatch.setenv("AQR_PIPE_SCHED", sched)
+    ip, ix, dv = problems.laplacian5(640, 480, 1e-2)
+    m, n = 640 * 480, 21
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    Z = np.asfortranarray(problems.rng(9, 7).standard_normal((m, n)))
+    Zh = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
+    Zh.copy_(torch.from_numpy(Z))
+    for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row"):
+        rd = aqr.factorize(Zh.cuda(), op, meth)
+        for Zin in (Zh, Z):
+            rh = aqr.factorize(Zin, op, meth)
+            Qh = rh.Q if isinstance(rh.Q, np.ndarray) else rh.Q.numpy()
+            Rh = rh.R if isinstance(rh.R, np.ndarray) else rh.R.numpy()
+            assert np.array_equal(Qh, rd.Q.cpu().numpy()) and np.array_equal(Rh, rd.R.cpu().numpy()), (meth, sched)
+
+
 def test_host_c_entry_matches_device_path(aqr):
     """aqr_gs_factor_host (numpy buffers, int64 CSR)."""
     import ctypes

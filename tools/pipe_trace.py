@@ -28,3 +28,13 @@ print(f"{meth}: wall {1e3 * (t1 - t0):.2f} ms, {len(t)} traced launches, first s
 gaps = [(i, (start[i] - end[i - 1]) / 1e3, (start[i] - base) / 1e6) for i in range(1, len(t)) if start[i] - end[i - 1] > 20000]
 for i, g, at in gaps:
     print(f"  idle {g:8.1f} us before launch {i} at {at:.2f} ms")
+dur = (end - start) / 1e3
+print(f"  launches by duration: >200us {int((dur > 200).sum())}, median {np.median(dur):.1f} us; "
+      f"last kernel end {(end[-1] - base) / 1e6:.2f} ms after first start")
+# where the busy time goes: first / second half of the span
+half = base + (end[-1] - base) // 2
+print(f"  busy in first half {dur[start < half].sum() / 1e3:.2f} ms, second half {dur[start >= half].sum() / 1e3:.2f} ms")
+for i in range(len(t)):
+    if dur[i] > 60 or (i > 0 and start[i] - end[i - 1] > 20000):
+        print(f"  launch {i:3d} start {(start[i] - base) / 1e6:6.2f} ms dur {dur[i]:7.1f} us"
+              f" gap-before {(start[i] - end[i - 1]) / 1e3 if i else 0:7.1f} us")
