@@ -662,18 +662,18 @@ struct HostOut {
     cudaEvent_t ev = nullptr;
 };
 
-int catchup_mode() {  // AQR_CATCHUP=0: one trailing launch (+ totals) per caught-up step (A/B)
-    static const int v = [] {
-        const char *e = std::getenv("AQR_CATCHUP");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
+// AQR_CATCHUP=0: one trailing launch (+ totals) per caught-up step; 2: the
+// cooperative launch with two grid barriers per step (A/B; read per call)
+int catchup_mode() {
+    const char *e = std::getenv("AQR_CATCHUP");
+    return e ? std::atoi(e) : 1;
 }
 
 template <int RPT, bool HP, bool CGS>
 aqr_status launch_catchup_t(const aqr::CatchArgs &c, cudaStream_t s) {
+    // wsum [kWarps][2] + the redundant totals rs[w] (rounded up to 8: block_totals<8>)
     constexpr int kCu = HP ? 1 : 2;  // columns per unit (catchup_kernel)
-    const size_t smem = sizeof(double) * aqr::kWarps * kCu;
+    const size_t smem = sizeof(double) * (2 * aqr::kWarps + (c.redundant ? ((c.w + 7) / 8) * 8 : 0));
     AQR_TRY(ensure_smem(aqr::catchup_kernel<RPT, HP, CGS>, smem));
     int o = 0;
     AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, aqr::catchup_kernel<RPT, HP, CGS>, aqr::kBlock, smem));
@@ -819,6 +819,9 @@ struct Run {
             c.partial = pp->partial2;
             c.status = status;
             c.trace = trace_slot();
+            // one barrier per step when the totals fit in shared memory
+            // (partial2 holds two parity buffers of the widest chunk)
+            c.redundant = (catchup_mode() != 2 && w <= 4096) ? 1 : 0;
             AQR_TRY(launch_catchup(c, hp, cgs, s));
             live = c1;
             return AQR_OK;
@@ -1215,12 +1218,9 @@ static void keep_pool_memory() {
 // chunks at the start let the first steps -- and the D2H of Q -- begin
 // earlier; small ones at the end shorten the tail after the last H2D
 // (catch-up of the last chunk, its steps and the D2H of its columns).
-int pipe_sched_mode() {
-    static const int v = [] {
-        const char *e = std::getenv("AQR_PIPE_SCHED");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
+int pipe_sched_mode() {  // read per call
+    const char *e = std::getenv("AQR_PIPE_SCHED");
+    return e ? std::atoi(e) : 0;
 }
 
 std::vector<int64_t> pipe_bounds(int64_t n, int64_t chunk_cols) {
@@ -1297,7 +1297,8 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
     const int64_t ntiles = std::max<int64_t>(aqr::num_tiles(m), 1);
     keep_pool_memory();
     AQR_CUDA(cudaMallocAsync((void **)&pp.vall, 8 * (size_t)m * n, s));
-    AQR_CUDA(cudaMallocAsync((void **)&pp.partial2, 8 * (size_t)n * ntiles, s));
+    // two parity buffers of up to n columns, + 8 columns read past the end by block_totals<8>
+    AQR_CUDA(cudaMallocAsync((void **)&pp.partial2, 8 * (2 * (size_t)n + 8) * ntiles, s));
     SideCtx h2d;
     AQR_TRY(side_acquire(h2d));
     aqr_status st = AQR_OK;

@@ -249,8 +249,12 @@ __device__ __forceinline__ void norm_finish_dev(int64_t i, double t, double zz, 
 __device__ __forceinline__ bool last_block(unsigned *counter, unsigned expected) {
     __shared__ unsigned ticket;
     if (threadIdx.x == 0) {
-        __threadfence();
-        ticket = atomicAdd(counter, 1u);
+        // release: thread 0's partial stores are ordered before the ticket
+        // (the other warps' stores are consumed by the next kernel only);
+        // cheaper than a full fence.sc, which also waits for those
+        unsigned tk;
+        asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(tk) : "l"(counter) : "memory");
+        ticket = tk;
     }
     __syncthreads();
     const bool last = ticket == expected - 1;
@@ -547,6 +551,13 @@ __device__ __forceinline__ void trail_vectors(const TrailArgs &a, int64_t row0, 
     }
 }
 
+// Columns per unit prefetched into L2 before the dependency wait (0: off;
+// build-time knob -DAQR_TRAIL_PREFETCH=k for A/B).
+#ifndef AQR_TRAIL_PREFETCH
+#define AQR_TRAIL_PREFETCH 4
+#endif
+constexpr int trail_prefetch_cols = AQR_TRAIL_PREFETCH;
+
 // One (tile, column group) work unit of the trailing pass (all kBlock threads).
 template <int RPT, int CU, bool HP, bool CGS>
 __device__ __forceinline__ void trail_body(const TrailArgs &a, int tile, int group, double *wsum) {
@@ -615,9 +626,35 @@ __device__ __forceinline__ void trail_body(const TrailArgs &a, int tile, int gro
     }
 }
 
+// Before the grid-dependency wait: bring this unit's q_{i-1} tile and its
+// first columns' tiles (16 KB each, written by the kernel before the
+// previous one) into L2 with bulk prefetches, so the first loads after the
+// wait hit L2 while the previous kernel drains.  L2 is the coherence point:
+// a prefetch never makes a later load stale.
+template <int RPT>
+__device__ __forceinline__ void trail_prefetch(const TrailArgs &a, int tile, int group) {
+    if (RPT != 8 || threadIdx.x != 0 || trail_prefetch_cols <= 0) return;
+    const int64_t row0 = (int64_t)tile * (kBlock * RPT);
+    const int64_t rows = min((int64_t)kBlock * RPT, a.m - row0);
+    const uint32_t bytes = (uint32_t)(rows * 8) & ~15u;
+    if (bytes == 0) return;
+    auto pf = [&](const double *base) {
+        if (((uintptr_t)base & 15) == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base), "r"(bytes) : "memory");
+    };
+    const int cbeg = a.jbeg + group * a.cpg;
+    const int cend = min(a.jend, cbeg + min(a.cpg, trail_prefetch_cols));
+    const double *zb = a.Wsrc ? a.Wsrc : a.W;
+    const int64_t ld = a.Wsrc ? a.ldwsrc : a.ldw;
+    if (a.qprev) pf(a.qprev + row0);
+    for (int j = cbeg; j < cend; ++j) pf(zb + (int64_t)j * ld + row0);
+}
+
 template <int RPT, int CU, bool HP, bool CGS>
 __global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
     trace_mark(a.trace, 0);
+    trail_prefetch<RPT>(a, a.reverse ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x,
+                        a.reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y);
     pdl_wait();
     trace_mark(a.trace, 1);
     if (failed(a.status)) return;
@@ -654,9 +691,10 @@ struct CatchArgs {
     const double *vall;  // per-step vectors, ld m: HA x_k (p_k = x_k / r_kk), HP / naive p_k
     int32_t p_direct;
     double *Rt;       // n x n row-major
-    double *partial;  // [w][ntiles]
+    double *partial;  // [w][ntiles] (x 2 when redundant: by step parity)
     const int32_t *status;
-    int32_t trace;    // AQR_TRACE builds: launch slot (-1 off)
+    int32_t trace;      // AQR_TRACE builds: launch slot (-1 off)
+    int32_t redundant;  // per-CTA totals, one grid barrier per step (smem: w doubles)
 };
 
 template <int RPT, bool HP, bool CGS>
@@ -666,12 +704,28 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
     trace_mark(a.trace, 0);
     trace_mark(a.trace, 1);
     if (failed(a.status)) return;  // uniform: set before this launch
-    extern __shared__ double wsum[];  // [kWarps][CU]
+    extern __shared__ double wsum[];  // [kWarps][2], then rs[w] (redundant totals)
+    double *rs = wsum + 2 * kWarps;
     __shared__ double tot1[1];
     __shared__ double sm1[kWarps];
+    __shared__ double sm8[8 * kWarps];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // a.redundant: every CTA forms the w totals of step k-1 it needs itself
+    // (same block_totals tree; CTA 0 stores them to R), partials alternate
+    // between two buffers by step parity -- one grid barrier per step
+    // instead of two around a totals phase on w CTAs.
+    const int64_t pstride = (int64_t)a.w * a.ntiles;
     for (int k = 0; k < a.k1; ++k) {
         const bool upd = k > 0;
+        double *part = a.partial + (a.redundant ? (int64_t)(k & 1) * pstride : 0);
+        if (a.redundant && upd) {
+            const double *prev = a.partial + (int64_t)((k - 1) & 1) * pstride;
+            for (int cb = 0; cb < a.w; cb += 8) {
+                block_totals<8>(prev + (int64_t)cb * a.ntiles, a.ntiles, a.ntiles, rs + cb, sm8, SyncAll());
+            }
+            if (blockIdx.x == 0)
+                for (int c = threadIdx.x; c < a.w; c += kBlock) a.Rt[(int64_t)(k - 1) * a.n + a.c0 + c] = rs[c];
+        }
         const double rii = a.p_direct ? 1.0 : __ldcg(a.Rt + (int64_t)k * a.n + k);
         const double *qprev = upd ? a.W + (int64_t)(k - 1) * a.ldw : nullptr;
         const double *psrc = a.vall + (int64_t)k * a.m;
@@ -718,7 +772,8 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
                 for (int c = 0; c < CU; ++c) {
                     const int j = a.c0 + c0 + c;
                     const bool cj = c0 + c < a.w;
-                    const double rj = (cj && upd) ? __ldcg(a.Rt + (int64_t)(k - 1) * a.n + j) : 0.0;
+                    const double rj = (cj && upd) ? (a.redundant ? rs[c0 + c] : __ldcg(a.Rt + (int64_t)(k - 1) * a.n + j))
+                                                  : 0.0;
                     acc[c] = 0.0;
 #pragma unroll
                     for (int v = 0; v < RPT; ++v) {
@@ -747,16 +802,17 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
                 double s = wsum[c];
 #pragma unroll
                 for (int w2 = 1; w2 < kWarps; ++w2) s = __dadd_rn(s, wsum[w2 * CU + c]);
-                a.partial[(int64_t)(c0 + c) * a.ntiles + tile] = s;
+                part[(int64_t)(c0 + c) * a.ntiles + tile] = s;
             }
             __syncthreads();
         }
         grid.sync();
+        if (a.redundant && k + 1 < a.k1) continue;  // the next step forms these totals
         for (int cc = blockIdx.x; cc < a.w; cc += gridDim.x) {
-            block_totals<1>(a.partial + (int64_t)cc * a.ntiles, a.ntiles, a.ntiles, tot1, sm1, SyncAll());
+            block_totals<1>(part + (int64_t)cc * a.ntiles, a.ntiles, a.ntiles, tot1, sm1, SyncAll());
             if (threadIdx.x == 0) a.Rt[(int64_t)k * a.n + a.c0 + cc] = tot1[0];
         }
-        grid.sync();
+        if (!a.redundant) grid.sync();
     }
     trace_mark(a.trace, 2);
 }

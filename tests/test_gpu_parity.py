@@ -297,17 +297,20 @@ def test_pinned_host_input_streams_q_bitwise(aqr, meth, chunk, monkeypatch):
     assert rh.cost.mv_count == rd.cost.mv_count
 
 
-@pytest.mark.parametrize("sched", ["0", "1", "2"])
-def test_pipeline_chunk_schedules_bitwise(aqr, sched, monkeypatch):
+@pytest.mark.parametrize("sched,catchup", [("0", "1"), ("1", "1"), ("2", "1"), ("0", "2"), ("1", "0")])
+def test_pipeline_chunk_schedules_bitwise(aqr, sched, catchup, monkeypatch):
     """Every chunk schedule of the host-input pipeline (aqr_pipe_chunks:
-    uniform, tapered, ramped + tapered) -- catch-up launches over chunks of
+    uniform, tapered, ramped + tapered) and every catch-up form (one
+    cooperative launch with one grid barrier per step and per-CTA totals;
+    with two barriers around a totals phase; per-step launches) -- chunks of
     1 .. n/8 columns, balanced (tile, column) unit ranges -- gives the
     device-resident bits, for numpy (staged) and page-locked inputs."""
     import torch
 
-    from paper_1703_10440_b200 import _lib, problems
+    from paper_1703_10440_b200 import problems
 
     monkeypatch.setenv("AQR_PIPE_SCHED", sched)
+    monkeypatch.setenv("AQR_CATCHUP", catchup)
     ip, ix, dv = problems.laplacian5(640, 480, 1e-2)
     m, n = 640 * 480, 21
     op = aqr.CsrSpdOperator(ip, ix, dv)
