@@ -141,8 +141,7 @@ void timer_end(long idx, cudaStream_t s) {
     cudaEventRecord(g_timer.recs[(size_t)idx].e1, s);
 }
 
-// Experiment knob (read once): AQR_TRAIL_VARIANT = 0 TMA + L2 evict-first
-// hint (default), 1 TMA without hint, 2 generic LDG kernel.
+// Experiment knob (read once): AQR_TRAIL_VARIANT (see launch_trailing).
 int trail_variant() {
     static const int v = [] {
         const char *e = std::getenv("AQR_TRAIL_VARIANT");
@@ -455,7 +454,8 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     // Measured on B200 (tools/kernel_ab.py, config 2): the short-lived LDG
     // kernel plus a separate totals launch beats the persistent TMA-pipelined
     // kernel for HA (8.84 vs 9.26 ms/factorization) and HP (14.1 vs 14.4 ms).
-    // AQR_TRAIL_VARIANT: 0 = LDG CU=2 (default), 3 = LDG CU=4 (HA),
+    // AQR_TRAIL_VARIANT: 0 = LDG, CU=2 (HA) / CU=1 (HP) (default), 3 = LDG CU=4 (HA),
+    // 5 = LDG CU=1 (HA), 6 = LDG CU=2 (HP),
     // 1 = TMA without the L2 hint, 4 = TMA with the evict-first hint.
     const int tv = trail_variant();
     const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && (tv == 1 || tv == 4) && a.Wsrc == nullptr;
@@ -501,7 +501,12 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
         launch_pdl(aqr::trailing_kernel<RPT, CU, HP, CGS>, grid, aqr::kBlock, smem, s, a); \
     } while (0)
         if (big) {
-            if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
+            // MGS-HP: one column per iteration (128 registers, 2 CTAs/SM) measured
+            // 2.8 % faster than two (164 registers, 1 CTA/SM) on config 2;
+            // CGS-HP (144 registers either way: 1 CTA/SM) keeps two (12 % faster)
+            if (hp && (cgs || tv == 6)) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
+            else if (hp) LAUNCH(8, 1, true, false);
+            else if (tv == 5) { if (cgs) LAUNCH(8, 1, false, true); else LAUNCH(8, 1, false, false); }
             else if (tv == 3) { if (cgs) LAUNCH(8, 4, false, true); else LAUNCH(8, 4, false, false); }
             else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
         } else {

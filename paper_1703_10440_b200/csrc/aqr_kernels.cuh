@@ -650,8 +650,12 @@ __device__ __forceinline__ void trail_prefetch(const TrailArgs &a, int tile, int
     for (int j = cbeg; j < cend; ++j) pf(zb + (int64_t)j * ld + row0);
 }
 
+// HP trailing kernels: minimum resident CTAs per SM (build-time A/B knob)
+#ifndef AQR_HP_MINB
+#define AQR_HP_MINB 1
+#endif
 template <int RPT, int CU, bool HP, bool CGS>
-__global__ void __launch_bounds__(kBlock) trailing_kernel(TrailArgs a) {
+__global__ void __launch_bounds__(kBlock, HP ? AQR_HP_MINB : 1) trailing_kernel(TrailArgs a) {
     trace_mark(a.trace, 0);
     trail_prefetch<RPT>(a, a.reverse ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x,
                         a.reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y);

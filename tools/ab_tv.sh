@@ -1,0 +1,6 @@
+# A/B of trailing-kernel variants (AQR_TRAIL_VARIANT), alternating
+meth=$1; shift
+for rep in 1 2; do for tv in "$@"; do
+  printf "%-10s tv=%s " "$meth" "$tv"
+  AQR_TRAIL_VARIANT=$tv python tools/kernel_ab.py $meth | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('step %.3f ms  trailing %.3f ms' % (d['step_ms'], d['trailing']['ms_per_fact']))"
+done; done
