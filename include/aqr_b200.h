@@ -137,7 +137,8 @@ AQR_API aqr_status aqr_gs_factor_d2h(aqr_factor_args *args, double *Q_host, int6
 
 /* Host Z in, host Q / R out, with both transfers overlapped with the
  * factorization (row orientation): Z is copied in chunks of `chunk_cols`
- * columns (0 = ceil(n/8)) on an internal stream; when `ready` (page-locked
+ * columns (0 = the library's schedule, see aqr_pipe_chunks) on an internal
+ * stream; when `ready` (page-locked
  * host memory) is given, chunk c is copied only once *ready >= c + 1, so the
  * caller can still be writing later chunks into Z_host (a GPU-side stream
  * wait; the caller advances *ready in chunk order); the step loop brings a chunk in
