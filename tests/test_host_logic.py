@@ -106,6 +106,49 @@ def test_c_abi_library_exports_every_header_symbol():
     assert L.aqr_status_bytes(50) == 16 + 4 * 50
 
 
+def _pipe_chunks(n, chunk, sched=None):
+    code = (
+        "import numpy as np, sys\n"
+        "from paper_1703_10440_b200 import _lib\n"
+        "L = _lib.load(require_device=False)\n"
+        f"b = np.zeros({n} + 1, dtype=np.int64)\n"
+        f"k = L.aqr_pipe_chunks({n}, {chunk}, b.ctypes.data, {n} + 1)\n"
+        "print(' '.join(str(int(v)) for v in b[: k + 1]))\n"
+    )
+    import subprocess
+    import sys
+
+    env = dict(os.environ)
+    env.pop("AQR_PIPE_SCHED", None)
+    if sched is not None:
+        env["AQR_PIPE_SCHED"] = str(sched)
+    out = subprocess.run([sys.executable, "-c", code], env=env, check=True, capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    return [int(v) for v in out.stdout.split()]
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 9, 64, 100, 256])
+def test_pipeline_chunk_schedule(n):
+    """aqr_pipe_chunks (host logic, no device): boundaries 0 .. n strictly
+    increasing; chunk_cols > 0 gives uniform chunks; the default schedule is
+    ceil(n/8)-column chunks; the tapered schedule halves towards the end and
+    the ramped one also starts with ceil(n/8)/4 columns."""
+    w = max(1, (n + 7) // 8)
+    for sched in (None, 1, 2):
+        b = _pipe_chunks(n, 0, sched)
+        assert b[0] == 0 and b[-1] == n and all(x < y for x, y in zip(b, b[1:])), (sched, b)
+        widths = [y - x for x, y in zip(b, b[1:])]
+        assert max(widths) <= w, (sched, b)
+        if sched is None:
+            assert widths == [w] * (n // w) + ([n % w] if n % w else []), b
+        if sched == 1 and n > w:
+            assert widths[-1] == 1 and widths[: (n - w) // w] == [w] * ((n - w) // w), b
+        if sched == 2 and w >= 4 and n > 2 * w:
+            assert widths[0] == w // 4, b
+    b = _pipe_chunks(n, 3, 1)  # explicit chunk width: uniform whatever the schedule
+    assert b == list(range(0, n, 3)) + [n], b
+
+
 def test_ctypes_struct_layout_matches_header():
     # aqr_op / aqr_factor_args as declared in include/aqr_b200.h (LP64)
     assert ctypes.sizeof(_lib.AqrOp) == 4 + 4 + 8 + 8 + 8 + 8 * 3 + 8 + 8 * 3 + 8
