@@ -317,7 +317,7 @@ def test_pipeline_chunk_schedules_bitwise(aqr, sched, catchup, monkeypatch):
     Z = np.asfortranarray(problems.rng(9, 7).standard_normal((m, n)))
     Zh = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
     Zh.copy_(torch.from_numpy(Z))
-    for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row"):
+    for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "cgs-hp-row", "mgs-naive-row"):
         rd = aqr.factorize(Zh.cuda(), op, meth)
         for Zin in (Zh, Z):
             rh = aqr.factorize(Zin, op, meth)
