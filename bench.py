@@ -250,7 +250,7 @@ def run_b200(args, rank, world, local_rank):
     traffic, traffic_src = None, None
     import glob
 
-    for tpath in sorted(glob.glob(os.path.join(REPO, "profiles", "r*", "trailing_traffic.json")))[::-1]:
+    for tpath in sorted(glob.glob(os.path.join(REPO, "profiles", "r*", "trailing_traffic*.json")))[::-1]:
         with open(tpath) as f:
             tt = json.load(f)
         if tt.get("method") == args.method and tt.get("traffic_over_algorithmic") and nl.value:

@@ -26,12 +26,17 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 M, N = 1024 * 1024, 64
 
 
+HP = os.environ.get("NCU_METHOD", "mgs-ha-row") == "mgs-hp-row"
+
+
 def trailing_alg_bytes(step):
-    """Algorithmic bytes of the fused trailing pass at step i (HA, config 2)."""
+    """Algorithmic bytes of the fused trailing pass at step i (config 2;
+    HA, or HP with NCU_METHOD=mgs-hp-row: X carried and updated too), as
+    the library's trailing_bytes() counts them."""
     t = N - 1 - step
     upd = step > 0
-    per_col = 8 + (8 if upd else 0)
-    vec = 8 + (8 if upd else 0) + 16
+    per_col = 8 + (8 if upd else 0) + (16 if HP and upd else 0)
+    vec = 8 + (8 if upd else 0) + (8 if HP and upd else 0) + 16 + (8 if HP else 0)
     return M * (t * per_col + vec)
 
 
@@ -59,8 +64,15 @@ def raw(path):
     recs = []
     for r in rows[2:]:
         d = {h: r[i] for i, h in enumerate(hdr)}
+        d["__units__"] = dict(zip(hdr, units))
         recs.append(d)
     return recs
+
+
+def mbytes(d, k):
+    """A byte metric in MB whatever unit ncu chose for it (byte .. Gbyte)."""
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
+    return f(d, k) * scale.get(d.get("__units__", {}).get(k, "Mbyte"), 1.0)
 
 
 def f(d, k):
@@ -78,7 +90,7 @@ def main():
     tot = sum(v[1] for v in agg.values())
     lines = [f"# ncu summary — {rnd}", "",
              "Command: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e` "
-             "(config 2, mgs-ha-row, m = 1,048,576, n = 64) on one B200, "
+             f"(config 2, {'mgs-hp-row' if HP else 'mgs-ha-row'}, m = 1,048,576, n = 64) on one B200, "
              "`--clock-control none`.", "",
              "## Launch list of one factorization (cold-cache, serialised: compare shares)", "",
              "| kernel | launches | total µs | share |", "|---|---|---|---|"]
@@ -97,8 +109,8 @@ def main():
         for j, d in enumerate(raw(rep)):
             name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "")
             us = f(d, "gpu__time_duration.sum")
-            rd = f(d, "dram__bytes_read.sum")
-            wr = f(d, "dram__bytes_write.sum")
+            rd = mbytes(d, "dram__bytes_read.sum")
+            wr = mbytes(d, "dram__bytes_write.sum")
             launch = s0 + j
             step = launch - 64 if "trailing" in name else launch - 64
             alg = trailing_alg_bytes(step) if "trailing" in name else float("nan")
@@ -115,10 +127,11 @@ def main():
     mean_ratio = sum(r["ratio"] for r in ratios) / len(ratios) if ratios else None
     lines += ["", f"Mean DRAM traffic / algorithmic bytes of the captured trailing launches: "
               f"{mean_ratio:.3f}" if mean_ratio else ""]
-    with open(os.path.join(outdir, "ncu_summary.md"), "w") as fh:
+    sfx = "_hp" if HP else ""
+    with open(os.path.join(outdir, f"ncu_summary{sfx}.md"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    with open(os.path.join(outdir, "trailing_traffic.json"), "w") as fh:
-        json.dump({"method": "mgs-ha-row", "config": "config2", "launches": ratios,
+    with open(os.path.join(outdir, f"trailing_traffic{sfx}.json"), "w") as fh:
+        json.dump({"method": "mgs-hp-row" if HP else "mgs-ha-row", "config": "config2", "launches": ratios,
                    "traffic_over_algorithmic": mean_ratio}, fh, indent=1)
     print("\n".join(lines))
 
