@@ -183,26 +183,28 @@ __device__ __forceinline__ double block_sum(double v, double *smem /* kWarps */)
 // share (__syncthreads, or a named barrier in warp-specialized kernels).
 // Loads are issued 4 per chain ahead of the adds, so even 8192 tiles cost
 // only a few dependent L2 round trips.
-template <int NC, typename Bar>
+// H: tiles per column loaded together per iteration (registers vs round
+// trips; the sum order -- ascending t -- does not depend on it).
+template <int NC, typename Bar, int H = 4>
 __device__ __forceinline__ void block_totals(const double *p, int64_t stride, int32_t n,
                                              double *out /* smem or global, NC */,
                                              double *sm /* NC * kWarps */, Bar bar) {
     double acc[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-    for (int t0 = threadIdx.x; t0 < n; t0 += 4 * kBlock) {
-        double v[NC][4];
+    for (int t0 = threadIdx.x; t0 < n; t0 += H * kBlock) {
+        double v[NC][H];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
+            for (int h = 0; h < H; ++h) {
                 const int t = t0 + h * kBlock;
                 v[c][h] = t < n ? __ldcg(p + c * stride + t) : 0.0;
             }
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
-            for (int h = 0; h < 4; ++h)
+            for (int h = 0; h < H; ++h)
                 if (t0 + h * kBlock < n) acc[c] = __dadd_rn(acc[c], v[c][h]);
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -701,8 +703,13 @@ struct CatchArgs {
     int32_t redundant;  // per-CTA totals, one grid barrier per step (smem: w doubles)
 };
 
+// Tiles per column loaded together by the catch-up's per-CTA totals (build
+// knob: 2 keeps 2 CTAs/SM with a few spilled bytes; 1 no spills, two round trips).
+#ifndef AQR_CATCHUP_TOT_H
+#define AQR_CATCHUP_TOT_H 2
+#endif
 template <int RPT, bool HP, bool CGS>
-__global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
+__global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     trace_mark(a.trace, 0);
@@ -725,7 +732,8 @@ __global__ void __launch_bounds__(kBlock) catchup_kernel(CatchArgs a) {
         if (a.redundant && upd) {
             const double *prev = a.partial + (int64_t)((k - 1) & 1) * pstride;
             for (int cb = 0; cb < a.w; cb += 8) {
-                block_totals<8>(prev + (int64_t)cb * a.ntiles, a.ntiles, a.ntiles, rs + cb, sm8, SyncAll());
+                block_totals<8, SyncAll, AQR_CATCHUP_TOT_H>(prev + (int64_t)cb * a.ntiles, a.ntiles, a.ntiles, rs + cb, sm8,
+                                            SyncAll());
             }
             if (blockIdx.x == 0)
                 for (int c = threadIdx.x; c < a.w; c += kBlock) a.Rt[(int64_t)(k - 1) * a.n + a.c0 + c] = rs[c];
