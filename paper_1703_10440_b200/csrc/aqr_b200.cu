@@ -422,11 +422,24 @@ double trailing_bytes(const aqr::TrailArgs &a, bool hp, bool cgs) {
     return m * (t * per_col + vec);
 }
 
-// Generic kernel: column groups so that ~4 CTAs per SM are in flight.
+// Generic kernel: column groups so that ~trail_ctas_per_sm() CTAs per SM are in flight.
 constexpr int kMaxCpg = 256;
+// CTAs per SM the column grouping aims at (AQR_TRAIL_CTAS for A/B).  Columns
+// are split into groups only when the tiles alone give fewer CTAs: on config
+// 2 (512 tiles) one group per tile -- each CTA walks all t columns and reads
+// the step vectors once -- beat two groups by 2.8 % (HA 7.51 -> 7.30 ms) and
+// 2 % (HP 12.59 -> 12.34 ms); 2 and 3 give the same grouping there.
+int trail_ctas_per_sm() {
+    static const int v = [] {
+        const char *e = std::getenv("AQR_TRAIL_CTAS");
+        return e ? std::max(1, std::atoi(e)) : 3;
+    }();
+    return v;
+}
+
 int choose_cpg_generic(int64_t ntiles, int64_t ncols) {
     if (ncols <= 0) return 1;
-    const int64_t want_ctas = (int64_t)sm_count() * 4;
+    const int64_t want_ctas = (int64_t)sm_count() * trail_ctas_per_sm();
     int64_t groups = std::max<int64_t>(1, (want_ctas + ntiles - 1) / ntiles);
     groups = std::min<int64_t>(groups, ncols);
     int64_t cpg = (ncols + groups - 1) / groups;
