@@ -1460,6 +1460,113 @@ __device__ __forceinline__ bool csr_step_body_pf(const CsrArgs &a, int64_t cta, 
     return true;
 }
 
+// Deeper pipeline (default; build knob AQR_SPMV_PF2 = 2: L2, 1: L1, 0: the
+// csr_step_body_pf form): pointers three rows ahead, the entries of the row
+// after next prefetched into the cache, the next row's entries loaded into
+// registers (now a cache hit), and a row's X and q gathers all issued before
+// the arithmetic.  Config 2 HA 7.31 -> 7.20 ms, CGS-HA 9.45 -> 9.37-9.44 ms
+// (alternating builds, tools/ab_libs.sh); prefetching the next row's gathers
+// too was slower (spills).  Same rows, order and arithmetic as
+// csr_step_body_pf (bitwise equal).
+#ifndef AQR_SPMV_PF2
+#define AQR_SPMV_PF2 2
+#endif
+__device__ __forceinline__ void prefetch_entries(const CsrArgs &a, int s, int e) {
+    if (e <= s) return;
+    if (AQR_SPMV_PF2 == 1) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.indices + s));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.data + s));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(a.data + e - 1));
+    } else {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.indices + s));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.data + s));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.data + e - 1));
+    }
+}
+
+template <int B, bool PRE = false>
+__device__ __forceinline__ bool csr_step_body_pf2(const CsrArgs &a, int64_t cta, int64_t G) {
+    const bool upd = a.r != nullptr;
+    const int64_t nblk = (a.m + kBlock - 1) / kBlock;
+    const int64_t stride = G * kBlock;
+    double t = 0.0, zz = 0.0, xx = 0.0;
+    int64_t row = cta * kBlock + threadIdx.x;
+    int s = row < a.m ? __ldg(a.indptr + row) : 0;
+    int e = row < a.m ? __ldg(a.indptr + row + 1) : 0;
+    int64_t nrow = row + stride;
+    int ns = nrow < a.m ? __ldg(a.indptr + nrow) : 0;
+    int ne = nrow < a.m ? __ldg(a.indptr + nrow + 1) : 0;
+    int64_t n2 = nrow + stride;
+    int s2 = n2 < a.m ? __ldg(a.indptr + n2) : 0;
+    int e2 = n2 < a.m ? __ldg(a.indptr + n2 + 1) : 0;
+    int c[B];
+    double v[B];
+    load_entries<B>(a, s, e, c, v);
+    prefetch_entries(a, ns, ne);
+    if (PRE) {
+        pdl_wait();
+        if (failed(a.out.status)) return false;
+    }
+    const double rj = a.rin.partial ? rrow_first(a.rin, cta == 0) : (upd ? *a.r : 0.0);
+    for (int64_t blk = cta; blk < nblk; blk += G) {
+        // stage 0: pointers three rows ahead; stage 1: entries two rows ahead
+        // toward the cache; stage 2: entries of the next row into registers
+        const int64_t n3 = n2 + stride;
+        const int s3 = n3 < a.m ? __ldg(a.indptr + n3) : 0;
+        const int e3 = n3 < a.m ? __ldg(a.indptr + n3 + 1) : 0;
+        prefetch_entries(a, s2, e2);
+        int nc[B];
+        double nv[B];
+        load_entries<B>(a, ns, ne, nc, nv);
+        if (row < a.m) {
+            double y;
+            if (e - s <= B) {
+                double xv[B], qv[B];
+#pragma unroll
+                for (int h = 0; h < B; ++h) {
+                    const bool ok = s + h < e;
+                    xv[h] = ok ? __ldg(a.X + c[h]) : 0.0;
+                    qv[h] = (upd && ok) ? __ldg(a.qprev + c[h]) : 0.0;
+                }
+#pragma unroll
+                for (int h = 0; h < B; ++h)
+                    if (upd && s + h < e) xv[h] = __dsub_rn(xv[h], __dmul_rn(rj, qv[h]));
+                y = 0.0;
+#pragma unroll
+                for (int h = 0; h < B; ++h)
+                    if (s + h < e) y = __dadd_rn(y, __dmul_rn(v[h], xv[h]));
+            } else {
+                y = csr_row<B>(a, a.X, s, e, upd, rj);
+            }
+            double z = a.X[row];
+            if (upd) z = __dsub_rn(z, __dmul_rn(rj, a.qprev[row]));
+            a.Y[row] = y;
+            if (a.znew) a.znew[row] = z;
+            t = fma(z, y, t);
+            zz = fma(z, z, zz);
+            xx = fma(y, y, xx);
+        }
+        row = nrow;
+        s = ns;
+        e = ne;
+        nrow = n2;
+        ns = s2;
+        ne = e2;
+        n2 = n3;
+        s2 = s3;
+        e2 = e3;
+#pragma unroll
+        for (int h = 0; h < B; ++h) {
+            c[h] = nc[h];
+            v[h] = nv[h];
+        }
+    }
+    pdl_trigger();
+    norm_cta_partial(a.out, t, zz, xx, cta);
+    norm_last_cta(a.out, (unsigned)G);
+    return true;
+}
+
 // AQR_SPMV_PREWAIT=0: wait before any load (A/B; config 2 HA 7.60 vs 7.62 ms).
 #ifndef AQR_SPMV_PREWAIT
 #define AQR_SPMV_PREWAIT 1
@@ -1472,7 +1579,11 @@ __global__ void __launch_bounds__(kBlock, MINB) csr_step_pf_kernel(CsrArgs a) {
         if (failed(a.out.status)) return;
     }
     trace_mark(a.trace, 1);  // with PRE: before the wait
-    if (!csr_step_body_pf<B, AQR_SPMV_PREWAIT != 0>(a, blockIdx.x, gridDim.x)) return;
+    if (AQR_SPMV_PF2 != 0) {
+        if (!csr_step_body_pf2<B, AQR_SPMV_PREWAIT != 0>(a, blockIdx.x, gridDim.x)) return;
+    } else {
+        if (!csr_step_body_pf<B, AQR_SPMV_PREWAIT != 0>(a, blockIdx.x, gridDim.x)) return;
+    }
     rrow_rest(a.rin, blockIdx.x, gridDim.x);
     trace_mark(a.trace, 2);
 }
