@@ -384,14 +384,13 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
     trace_mark(a.trace, 1);
     if (failed(a.out.status)) return;
     const bool upd = a.r != nullptr;
-    const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x;
     double t = 0.0, zz = 0.0, xx = 0.0;
-    for (int64_t b0 = blockIdx.x; b0 < nblk; b0 += G * kColTiles) {
-        double z[kColTiles], xv[kColTiles], q[kColTiles], pp[kColTiles];
+    double z[kColTiles], xv[kColTiles], q[kColTiles], pp[kColTiles];
+    auto load = [&](int64_t b0) {  // loads first
 #pragma unroll
-        for (int g = 0; g < kColTiles; ++g) {  // loads first
+        for (int g = 0; g < kColTiles; ++g) {
             const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
             const bool ok = b0 + g * G < nblk && r < a.m;
             z[g] = ok ? (a.zsrc ? a.zsrc[r] : a.z[r]) : 0.0;
@@ -399,6 +398,13 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
             xv[g] = ok ? (a.x ? a.x[r] : (a.xnorm ? a.xnorm[r] : 0.0)) : 0.0;
             pp[g] = (ok && upd && a.x) ? a.pprev[r] : 0.0;
         }
+    };
+    // the first batch is in flight while the r-row total forms (it does not
+    // depend on r_{i-1,i})
+    if (blockIdx.x < nblk) load(blockIdx.x);
+    const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
+    for (int64_t b0 = blockIdx.x; b0 < nblk; b0 += G * kColTiles) {
+        if (b0 != blockIdx.x) load(b0);
 #pragma unroll
         for (int g = 0; g < kColTiles; ++g) {
             const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
