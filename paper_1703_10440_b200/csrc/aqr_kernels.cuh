@@ -718,6 +718,9 @@ struct CatchArgs {
 
 // Tiles per column loaded together by the catch-up's per-CTA totals (build
 // knob: 2 keeps 2 CTAs/SM with a few spilled bytes; 1 no spills, two round trips).
+#ifndef AQR_CATCHUP_REVERSE
+#define AQR_CATCHUP_REVERSE 1
+#endif
 #ifndef AQR_CATCHUP_TOT_H
 #define AQR_CATCHUP_TOT_H 2
 #endif
@@ -765,7 +768,12 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
         int cur = -1;
         double q[RPT], p[RPT], pp[RPT];
         bool ok[RPT];
-        for (int64_t u = ub; u < ue; ++u) {
+        // odd steps walk the range backwards: a step starts on the units the
+        // previous one touched last (still in L2); per unit independent, so
+        // the bits do not depend on the walk
+        const bool back = AQR_CATCHUP_REVERSE && (k & 1);
+        for (int64_t uu = ub; uu < ue; ++uu) {
+            const int64_t u = back ? ub + ue - 1 - uu : uu;
             const int tile = (int)(u / ng), c0 = (int)(u % ng) * CU;
             const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
             if (tile != cur) {
