@@ -1006,8 +1006,9 @@ aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, 
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
     const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
     if (aqr::rows_per_thread(a.m) == 8) {
-        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, 2, HP, CGS>, smem));
-        launch_pdl(aqr::p2p_trailing_kernel<8, 2, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
+        constexpr int CU = (HP && !CGS) ? 1 : 2;  // as launch_trailing: MGS-HP one column per iteration
+        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, CU, HP, CGS>, smem));
+        launch_pdl(aqr::p2p_trailing_kernel<8, CU, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
     } else {
         AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, smem));
         launch_pdl(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
@@ -1569,6 +1570,7 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
         t.partial = partial;
         t.status = status;
         t.trace = -1;
+        t.reverse = (int32_t)(i & 1);  // backwards on odd steps (L2 reuse, as the single-GPU pass)
         aqr_status st;
         if (hp) st = cgs ? launch_p2p_trailing<true, true>(t, P, i, Rt + i * n + i, status, s)
                          : launch_p2p_trailing<true, false>(t, P, i, Rt + i * n + i, status, s);

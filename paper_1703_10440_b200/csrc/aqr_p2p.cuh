@@ -175,16 +175,23 @@ __global__ void __launch_bounds__(kBlock, 3) p2p_csr_step_kernel(CsrArgs a, P2PA
     int64_t nrow = row + stride;
     int ns = nrow < a.m ? __ldg(a.indptr + nrow) : 0;
     int ne = nrow < a.m ? __ldg(a.indptr + nrow + 1) : 0;
+    int64_t n2 = nrow + stride;
+    int s2 = n2 < a.m ? __ldg(a.indptr + n2) : 0;
+    int e2 = n2 < a.m ? __ldg(a.indptr + n2 + 1) : 0;
     int c[B];
     double v[B];
     load_entries<B>(a, s, e, c, v);  // the operator is read-only: before the wait
+    prefetch_entries(a, ns, ne);
     pdl_wait();
     if (failed(a.out.status)) return;
     const double rj = p2p_rrow_in(p, i, Rt);
     for (int64_t blk = blockIdx.x; blk < nblk; blk += G) {
-        const int64_t n2 = nrow + stride;
-        const int s2 = n2 < a.m ? __ldg(a.indptr + n2) : 0;
-        const int e2 = n2 < a.m ? __ldg(a.indptr + n2 + 1) : 0;
+        // as csr_step_body_pf2: pointers three rows ahead, the entries of the
+        // row after next toward L2, the next row's entries into registers
+        const int64_t n3 = n2 + stride;
+        const int s3 = n3 < a.m ? __ldg(a.indptr + n3) : 0;
+        const int e3 = n3 < a.m ? __ldg(a.indptr + n3 + 1) : 0;
+        prefetch_entries(a, s2, e2);
         int nc[B];
         double nv[B];
         load_entries<B>(a, ns, ne, nc, nv);
@@ -215,6 +222,9 @@ __global__ void __launch_bounds__(kBlock, 3) p2p_csr_step_kernel(CsrArgs a, P2PA
         nrow = n2;
         ns = s2;
         ne = e2;
+        n2 = n3;
+        s2 = s3;
+        e2 = e3;
 #pragma unroll
         for (int h = 0; h < B; ++h) {
             c[h] = nc[h];
@@ -274,6 +284,11 @@ __global__ void __launch_bounds__(kBlock, 4) p2p_col_update_kernel(ColArgs a, P2
 template <int RPT, int CU, bool HP, bool CGS>
 __global__ void __launch_bounds__(kBlock) p2p_trailing_kernel(TrailArgs a, P2PArgs p, int64_t i, double *rii_out,
                                                               int32_t *status) {
+    // as trailing_kernel: odd steps walk the units backwards, and this
+    // unit's first tiles are prefetched into L2 before the dependency wait
+    const int tile = a.reverse ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+    const int group = a.reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
+    trail_prefetch<RPT>(a, tile, group);
     pdl_wait();
     if (failed(a.status)) return;
     extern __shared__ double wsum[];
@@ -293,7 +308,7 @@ __global__ void __launch_bounds__(kBlock) p2p_trailing_kernel(TrailArgs a, P2PAr
     if (!ok_sh) return;
     TrailArgs b = a;
     b.rii = &rii_sh;
-    trail_body<RPT, CU, HP, CGS>(b, blockIdx.x, blockIdx.y, wsum);
+    trail_body<RPT, CU, HP, CGS>(b, tile, group, wsum);
 }
 
 // Local R-row totals of step i (CTA c: column jbeg + c), sent to every rank;
