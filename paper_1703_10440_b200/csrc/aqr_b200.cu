@@ -1232,11 +1232,11 @@ static void keep_pool_memory() {
 }
 
 // Column chunks of the host-input pipeline: chunk_cols > 0 gives uniform
-// chunks; 0 the default schedule (AQR_PIPE_SCHED: 0 uniform n/8, 1 n/8 then
-// halving towards the end, 2 also ramping up from n/32 at the start).  Small
-// chunks at the start let the first steps -- and the D2H of Q -- begin
-// earlier; small ones at the end shorten the tail after the last H2D
-// (catch-up of the last chunk, its steps and the D2H of its columns).
+// chunks; 0 the default schedule, uniform n/8.  AQR_PIPE_SCHED selects the
+// measured alternatives (1: n/8 then halving towards the end, 2: also
+// ramping up from n/32 at the start): small final chunks still need a
+// catch-up over all previous steps each, small first ones start the D2H of
+// Q earlier, and neither beat uniform chunks.
 int pipe_sched_mode() {  // read per call
     const char *e = std::getenv("AQR_PIPE_SCHED");
     return e ? std::atoi(e) : 0;
