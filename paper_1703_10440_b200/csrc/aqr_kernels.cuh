@@ -36,7 +36,8 @@
 namespace aqr {
 
 // Columns of the register-resident-row SpMM in flight per thread (build knob;
-// config 2 HP block apply 536 / 480 / 497 us at 2 / 4 / 8)
+// config 2 HP block apply 366 / 352 / 582 us at 2 / 4 / 8 with the gathers of
+// a column block issued before its stores; 480 us before that)
 #ifndef AQR_SPMM_UNROLL
 #define AQR_SPMM_UNROLL 4
 #endif
@@ -1337,8 +1338,28 @@ __global__ void __launch_bounds__(kBlock) csr_row_kernel(CsrArgs a) {
                 c[h] = ok ? __ldg(a.indices + s + h) : 0;
                 val[h] = ok ? __ldg(a.data + s + h) : 0.0;
             }
-#pragma unroll kSpmmUnroll
-            for (int64_t col = 0; col < a.k; ++col) {
+            // kSpmmUnroll columns per block: all their gathers are issued
+            // before the first store (a store to Y could alias X as far as
+            // the compiler knows, which would serialize the columns)
+            int64_t col = 0;
+            for (; col + kSpmmUnroll <= a.k; col += kSpmmUnroll) {
+                double xv[kSpmmUnroll][B];
+#pragma unroll
+                for (int u = 0; u < kSpmmUnroll; ++u) {
+                    const double *x = a.X + (col + u) * a.ldx;
+#pragma unroll
+                    for (int h = 0; h < B; ++h) xv[u][h] = s + h < e ? __ldg(x + c[h]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kSpmmUnroll; ++u) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int h = 0; h < B; ++h)
+                        if (s + h < e) acc = __dadd_rn(acc, __dmul_rn(val[h], xv[u][h]));
+                    a.Y[row + (col + u) * a.ldy] = acc;
+                }
+            }
+            for (; col < a.k; ++col) {
                 const double *x = a.X + col * a.ldx;
                 double xv[B];
 #pragma unroll
