@@ -296,6 +296,26 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         return launched("csr_step_kernel");
     }
     const int32_t mr = op->max_row_nnz;
+    static const int plain_pf = [] {  // AQR_PLAIN_PF=0: plain SpMV on csr_row_kernel (A/B)
+        const char *e = std::getenv("AQR_PLAIN_PF");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (k == 1 && mr >= 1 && mr <= 8 && plain_pf != 0 && AQR_SPMV_PF2 != 0) {
+        // plain y = A x through the pipelined step kernel (no norms, no
+        // update): rows three deep instead of one dependent chain per row
+        const unsigned g1 = (unsigned)aqr::norm_tiles(op->m, false);
+        if (mr <= 4)
+            launch_pdl(aqr::csr_step_pf_kernel<4, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 5)
+            launch_pdl(aqr::csr_step_pf_kernel<5, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 6)
+            launch_pdl(aqr::csr_step_pf_kernel<6, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
+        else if (mr == 7)
+            launch_pdl(aqr::csr_step_pf_kernel<7, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
+        else
+            launch_pdl(aqr::csr_step_pf_kernel<8, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
+        return launched("csr_step_kernel");
+    }
     if (k > 1 && (mr > 8 || mr <= 0)) {  // long (or unknown) rows: CTA = (8 columns, 256 rows)
         const int64_t nb = (op->m + aqr::kBlock - 1) / aqr::kBlock;
         aqr::csr_spmm2_kernel<4, 8, 2><<<(unsigned)(((k + 7) / 8) * nb), aqr::kBlock, 0, s>>>(a);

@@ -1604,8 +1604,10 @@ __device__ __forceinline__ bool csr_step_body_pf2(const CsrArgs &a, int64_t cta,
         }
     }
     pdl_trigger();
-    norm_cta_partial(a.out, t, zz, xx, cta);
-    norm_last_cta(a.out, (unsigned)G);
+    if (a.out.npart != nullptr) {  // uniform; nullptr: plain y = A x (k = 1)
+        norm_cta_partial(a.out, t, zz, xx, cta);
+        norm_last_cta(a.out, (unsigned)G);
+    }
     return true;
 }
 

@@ -69,6 +69,7 @@ def default_factors(tmp_path_factory):
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},
     {"AQR_TRAIL_CTAS": "8"},
+    {"AQR_PLAIN_PF": "0"},
     {"AQR_CATCHUP": "2"},
     {"AQR_PIPE_SCHED": "2"},
     {"AQR_SPMV_VARIANT": "3"},
