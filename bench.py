@@ -102,6 +102,13 @@ class ClockSampler:
                  "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            # nvidia-smi takes a while to print its first sample: wait for it
+            # (up to 3 s) and drop it, so that the samples kept are the ones
+            # taken during the timed region that follows
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self
