@@ -146,11 +146,19 @@ AQR_API aqr_status aqr_gs_factor_d2h(aqr_factor_args *args, double *Q_host, int6
  * trailing passes and reduction trees: results are bitwise those of
  * aqr_gs_factor), and Q columns stream out as in aqr_gs_factor_d2h.  args->Q
  * is the device working matrix (Z is staged into it; args->Z is ignored);
- * Z_host / Q_host should be page-locked.  The column form copies Z in whole,
- * then runs aqr_gs_factor_d2h.  Returns after all copies completed. */
+ * Z_host / Q_host should be page-locked.  The workspace must hold
+ * aqr_workspace_bytes(...) + aqr_pipe_workspace_bytes(...) bytes (the
+ * pipeline's step vectors and catch-up partials follow the factorization's
+ * workspace; nothing is allocated inside).  The column form copies Z in
+ * whole, then runs aqr_gs_factor_d2h.  Returns after all copies completed. */
 AQR_API aqr_status aqr_gs_factor_pinned(aqr_factor_args *args, const double *Z_host, int64_t ldzh,
                                         double *Q_host, int64_t ldqh, double *R_host, int64_t ldrh,
                                         int64_t chunk_cols, const uint32_t *ready, void *stream);
+
+/* Extra workspace bytes of aqr_gs_factor_pinned beyond aqr_workspace_bytes:
+ * every step vector (m x n) and two parity buffers of catch-up partials. */
+AQR_API uint64_t aqr_pipe_workspace_bytes(int32_t family, int32_t variant, int32_t orientation, int64_t m,
+                                          int64_t n);
 
 /* Column chunks the host-input pipeline uses for n columns (chunk_cols as
  * passed to aqr_gs_factor_pinned; 0 = the library's schedule): writes the

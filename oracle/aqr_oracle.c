@@ -20,10 +20,12 @@
  * Layout: every matrix is column-major (Fortran) with leading dimension equal
  * to its row count, as aqr.operators.as_matrix produces (operators.py:28-33).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define UNIT_ROUNDOFF (1.0 / 9007199254740992.0) /* 2**-53, gram_schmidt.py:33 */
 
@@ -141,6 +143,20 @@ enum { AQRO_MGS = 0, AQRO_CGS = 1 };
 enum { AQRO_NAIVE = 0, AQRO_HA = 1, AQRO_HP = 2 };
 enum { AQRO_COL = 0, AQRO_ROW = 1 };
 
+/* Phase timers of the calling thread's last aqro_gs_factor (seconds):
+ * [0] the block apply (HP, gram_schmidt.py:136), [1] all normalize(j) calls
+ * (including their operator applies), [2] all project(i, j) calls.  Used
+ * only by bench.py to extrapolate a column-truncated CPU run to the full
+ * column count (each phase scales with its own call count). */
+static _Thread_local double g_phase[3];
+void aqro_last_phase_times(double *out) { memcpy(out, g_phase, sizeof g_phase); }
+
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
 typedef struct {
     int family, variant;
     int64_t m, n;
@@ -237,21 +253,32 @@ int64_t aqro_gs_factor(int family, int variant, int orientation, int64_t m, int6
     memset(Q, 0, mn * sizeof(double));
     memset(R, 0, (size_t)n * (size_t)n * sizeof(double));
     memset(flagged, 0, (size_t)n * sizeof(int32_t));
+    memset(g_phase, 0, sizeof g_phase);
+    double t0 = now_s(), t1;
     if (variant == AQRO_HP) { /* X = op.apply_block(Zw), gram_schmidt.py:136 */
         op_apply_block(&op, n, s.Zw, s.X);
         s.mv += n;
     }
+    g_phase[0] = now_s() - t0;
     int bad = 0;
     if (orientation == AQRO_COL) { /* gram_schmidt.py:167-171 */
         for (int64_t j = 0; j < n && !bad; ++j) {
+            t0 = now_s();
             for (int64_t i = 0; i < j; ++i) project(&s, i, j);
+            t1 = now_s();
             bad = normalize(&s, j);
+            g_phase[2] += t1 - t0;
+            g_phase[1] += now_s() - t1;
         }
     } else { /* gram_schmidt.py:172-176 */
         for (int64_t i = 0; i < n && !bad; ++i) {
+            t0 = now_s();
             bad = normalize(&s, i);
+            t1 = now_s();
+            g_phase[1] += t1 - t0;
             if (bad) break;
             for (int64_t j = i + 1; j < n; ++j) project(&s, i, j);
+            g_phase[2] += now_s() - t1;
         }
     }
     if (mv_count) *mv_count = s.mv;

@@ -48,6 +48,8 @@ def lib():
                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                 _d, ctypes.c_int, _d, _i64, _i64, _d, _d, _d, _i32, _i64, _d,
             ]
+            L.aqro_last_phase_times.restype = None
+            L.aqro_last_phase_times.argtypes = [_d]
             L.aqro_set_dot_mode.restype = None
             L.aqro_set_dot_mode.argtypes = [ctypes.c_int]
             L.aqro_householder_qr.restype = ctypes.c_int
@@ -140,6 +142,25 @@ def gs_factor(Z, op, method):
     if rc >= 0:
         raise OracleBreakdown(int(rc), fail.value)
     return OracleResult(Q, R, [int(j) for j in np.flatnonzero(flagged)], int(mv.value))
+
+
+def last_phase_times():
+    """(block apply, all normalize, all project) seconds of this thread's last gs_factor."""
+    out = np.zeros(3)
+    lib().aqro_last_phase_times(_p(out))
+    return tuple(float(v) for v in out)
+
+
+def extrapolate_seconds(phases, n_run, n_full):
+    """Full-width time from a column-truncated run (n_run columns -> n_full).
+
+    The block apply and the normalize steps scale with the column count, the
+    projections with the number of (i, j) pairs, n (n - 1) / 2; at fixed m
+    every call of one phase costs the same (gram_schmidt.py:136, 147-176)."""
+    apply_s, norm_s, proj_s = phases
+    lin = n_full / n_run
+    pairs = (n_full * (n_full - 1)) / max(n_run * (n_run - 1), 1)
+    return (apply_s + norm_s) * lin + proj_s * pairs
 
 
 def csr_matvec(indptr, indices, data, x):

@@ -1,5 +1,6 @@
 """In-tree build of libaqr_b200.so for sm_100a (``python -m paper_1703_10440_b200._build``)."""
 
+import glob
 import os
 import shutil
 import subprocess
@@ -8,8 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "aqr_b200.cu")]
-DEPENDS = SOURCES + [os.path.join(HERE, "csrc", "aqr_kernels.cuh"),
-                     os.path.join(REPO, "include", "aqr_b200.h")]
+DEPENDS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
+    os.path.join(REPO, "include", "aqr_b200.h")]
 OUT = os.path.join(HERE, "libaqr_b200.so")
 
 NVCC_FLAGS = [

@@ -72,6 +72,7 @@ class AqrP2PGroup(ctypes.Structure):
 # name -> (restype, argtypes); every symbol declared in include/aqr_b200.h
 SIGNATURES = {
     "aqr_workspace_bytes": (c_u64, [c_i32, c_i32, c_i32, c_i64, c_i64]),
+    "aqr_pipe_workspace_bytes": (c_u64, [c_i32, c_i32, c_i32, c_i64, c_i64]),
     "aqr_gs_factor": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp]),
     "aqr_p2p_exchange_bytes": (c_u64, [c_i64]),
     "aqr_p2p_alloc": (c_i32, [c_u64, ctypes.POINTER(c_vp)]),

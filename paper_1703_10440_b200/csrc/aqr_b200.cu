@@ -1025,6 +1025,7 @@ aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, 
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
     const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
+    const long tix = timer_begin(0, trailing_bytes(a, HP, CGS), s);
     if (aqr::rows_per_thread(a.m) == 8) {
         constexpr int CU = (HP && !CGS) ? 1 : 2;  // as launch_trailing: MGS-HP one column per iteration
         AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, CU, HP, CGS>, smem));
@@ -1033,6 +1034,7 @@ aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, 
         AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, smem));
         launch_pdl(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
     }
+    timer_end(tix, s);
     return launched("p2p_trailing_kernel");
 }
 
@@ -1232,23 +1234,21 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
 
 aqr_status aqr_gs_factor(aqr_factor_args *a, void *stream) { return gs_factor_impl(a, stream, nullptr); }
 
-// The pipeline's extra buffers come from the device's default stream-ordered
-// pool; keep freed blocks in the pool (release threshold = max) so repeated
-// calls do not map and unmap hundreds of MB each time.
-static void keep_pool_memory() {
-    static std::mutex mu;
-    static std::vector<int> done;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    std::lock_guard<std::mutex> lk(mu);
-    for (int d : done)
-        if (d == dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done.push_back(dev);
+// Extra workspace of the host-input pipeline (caller-owned, after the
+// factorization's own layout): vall (every step vector, m x n) and the
+// catch-up partials (two parity buffers of up to n columns, + 8 columns read
+// past the end by block_totals<8>).
+static void pipe_extra(int64_t m, int64_t n, uint64_t *vall_bytes, uint64_t *partial_bytes) {
+    const uint64_t ntiles = (uint64_t)std::max<int64_t>(aqr::num_tiles(m), 1);
+    *vall_bytes = al(8 * (uint64_t)m * (uint64_t)n);
+    *partial_bytes = al(8 * (2 * (uint64_t)n + 8) * ntiles);
+}
+
+uint64_t aqr_pipe_workspace_bytes(int32_t family, int32_t variant, int32_t orientation, int64_t m, int64_t n) {
+    (void)family, (void)variant, (void)orientation;
+    uint64_t a = 0, b = 0;
+    pipe_extra(std::max<int64_t>(m, 0), std::max<int64_t>(n, 0), &a, &b);
+    return a + b;
 }
 
 // Column chunks of the host-input pipeline: chunk_cols > 0 gives uniform
@@ -1333,11 +1333,15 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
     Pipe pp;
     pp.bounds = pipe_bounds(n, chunk_cols);
     const size_t nch = pp.bounds.size() - 1;
-    const int64_t ntiles = std::max<int64_t>(aqr::num_tiles(m), 1);
-    keep_pool_memory();
-    AQR_CUDA(cudaMallocAsync((void **)&pp.vall, 8 * (size_t)m * n, s));
-    // two parity buffers of up to n columns, + 8 columns read past the end by block_totals<8>
-    AQR_CUDA(cudaMallocAsync((void **)&pp.partial2, 8 * (2 * (size_t)n + 8) * ntiles, s));
+    {
+        const uint64_t base = layout(a->family, a->variant, a->orientation, m, n).total;
+        uint64_t vb = 0, pb = 0;
+        pipe_extra(m, n, &vb, &pb);
+        if (!a->workspace || a->workspace_bytes < base + vb + pb)
+            return set_err(AQR_ENOMEM, "workspace smaller than aqr_workspace_bytes() + aqr_pipe_workspace_bytes()");
+        pp.vall = at<double>(a->workspace, base);
+        pp.partial2 = at<double>(a->workspace, base + vb);
+    }
     SideCtx h2d;
     AQR_TRY(side_acquire(h2d));
     aqr_status st = AQR_OK;
@@ -1388,8 +1392,6 @@ aqr_status aqr_gs_factor_pinned(aqr_factor_args *a, const double *Z_host, int64_
     cudaStreamSynchronize(h2d.side);
     side_release(h2d);
     for (cudaEvent_t e : pp.ev) cudaEventDestroy(e);
-    cudaFreeAsync(pp.vall, s);
-    cudaFreeAsync(pp.partial2, s);
     if (cudaStreamSynchronize(s) != cudaSuccess && st == AQR_OK) st = set_err(AQR_ECUDA, "stream");
     return st;
 }

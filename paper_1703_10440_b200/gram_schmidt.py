@@ -204,7 +204,10 @@ def _gs_factor(Z, op, family, variant, orientation):
         Q = D.empty_f(m, n)
     R = D.empty_f(n, n)
     fam, var, ori = _lib.FAMILY_CODE[family], _lib.VARIANT_CODE[variant], _lib.ORIENTATION_CODE[orientation]
-    ws = t.empty(int(L.aqr_workspace_bytes(fam, var, ori, m, n)), dtype=t.uint8, device=Q.device)
+    wsb = int(L.aqr_workspace_bytes(fam, var, ori, m, n))
+    if host_in:  # the pipeline's step vectors and catch-up partials follow
+        wsb += int(L.aqr_pipe_workspace_bytes(fam, var, ori, m, n))
+    ws = t.empty(wsb, dtype=t.uint8, device=Q.device)
     flags = np.zeros(n, dtype=np.int32)
 
     native = _uses_native(op)

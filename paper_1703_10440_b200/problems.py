@@ -95,38 +95,63 @@ def config3(device=False):
     return _out((indptr, indices, data), Z, device)
 
 
-def _torch_gen(config, stream, device):
+def _torch_gen(config, stream, device, sub=None):
     import torch
 
-    ss = np.random.SeedSequence([1703, 10440, config, stream])
+    key = [1703, 10440, config, stream] + ([] if sub is None else [sub])
+    ss = np.random.SeedSequence(key)
     g = torch.Generator(device=device)
     g.manual_seed(int(ss.generate_state(1, dtype=np.uint64)[0] & ((1 << 63) - 1)))
     return g
 
 
-def config4(device=True, m=32768, n=256):
-    """Dense m = 32768, n = 256: A = B^T B / m + 0.1 I (B ~ N(0,1)), Z ~ N(0,1), on the GPU."""
+def config4(device=True, m=32768, n=256, rows=None):
+    """Dense m = 32768, n = 256: A = B^T B / m + 0.1 I (B ~ N(0,1)), Z ~ N(0,1), on the GPU.
+
+    ``rows = (r0, r1)`` returns only that row panel of A (all m columns) and
+    of Z -- what one rank of the row-partitioned run owns (Z rows exactly
+    those of the full Z; A's panel equal to the full A's rows up to the
+    rounding of the Gram product)."""
     import torch
 
     dev = torch.device("cuda")
+    r0, r1 = rows if rows is not None else (0, m)
     B = torch.randn((m, m), generator=_torch_gen(4, 0, dev), dtype=torch.float64, device=dev)
-    A = B.transpose(0, 1) @ B
-    del B
-    A /= m
-    A = 0.5 * (A + A.transpose(0, 1))
-    A.diagonal().add_(0.1)
-    Z = torch.randn((n, m), generator=_torch_gen(4, 1, dev), dtype=torch.float64, device=dev).t()
+    if rows is None:
+        A = B.transpose(0, 1) @ B
+        del B
+        A /= m
+        A = 0.5 * (A + A.transpose(0, 1))
+        A.diagonal().add_(0.1)
+    else:  # the panel of the symmetrised matrix, formed as the full one forms it
+        P = B[:, r0:r1].transpose(0, 1) @ B  # rows r0..r1 of B^T B
+        PT = (B.transpose(0, 1) @ B[:, r0:r1]).transpose(0, 1)  # rows r0..r1 of (B^T B)^T
+        del B
+        P /= m
+        PT /= m
+        A = 0.5 * (P + PT)
+        del P, PT
+        A[:, r0:r1].diagonal().add_(0.1)
+        A = A.t().contiguous().t()  # column-major panel, ld = r1 - r0
+    Z = torch.randn((n, m), generator=_torch_gen(4, 1, dev), dtype=torch.float64, device=dev)
+    Z = Z[:, r0:r1].contiguous().t() if rows is not None else Z.t()
     return A, Z
 
 
-def stencil27_device(n_side, shift, device):
-    """3-D 27-point stencil on n^3 (centre 26 + shift, neighbours -1), CSR int32 on the GPU."""
+def stencil27_device(n_side, shift, device, planes=None):
+    """3-D 27-point stencil on n^3 (centre 26 + shift, neighbours -1), CSR on the GPU.
+
+    ``planes = (z0, z1)`` builds only rows z0 n^2 .. z1 n^2 - 1 (whole grid
+    planes, what one rank of the row-partitioned run owns) with GLOBAL column
+    indices; indptr starts at 0.  Returns (indptr int64, indices int32,
+    values fp64)."""
     import torch
 
     n = n_side
     m = n ** 3
+    z0, z1 = planes if planes is not None else (0, n)
     dev = torch.device(device)
-    idx = torch.arange(m, device=dev, dtype=torch.int64)
+    idx = torch.arange(z0 * n * n, z1 * n * n, device=dev, dtype=torch.int64)
     iz, iy, ix = idx // (n * n), (idx // n) % n, idx % n
     cols, vals, valids = [], [], []
     for dz in (-1, 0, 1):
@@ -137,23 +162,55 @@ def stencil27_device(n_side, shift, device):
                 valids.append(v)
                 cols.append((idx + (dz * n + dy) * n + dx).to(torch.int32))
                 vals.append(26.0 + shift if (dz, dy, dx) == (0, 0, 0) else -1.0)
+    del iz, iy, ix
     valid = torch.stack(valids, dim=1)
+    del valids
     counts = valid.sum(dim=1)
-    indptr = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+    indptr = torch.zeros(idx.numel() + 1, dtype=torch.int64, device=dev)
     indptr[1:] = torch.cumsum(counts, 0)
     col = torch.stack(cols, dim=1)[valid]
-    val = torch.tensor(vals, dtype=torch.float64, device=dev).expand(m, 27)[valid]
+    del cols
+    val = torch.tensor(vals, dtype=torch.float64, device=dev).expand(idx.numel(), 27)[valid]
+    assert m < 2 ** 31
     return indptr, col, val
 
 
-def config5(device=True, n_side=256, n=256):
-    """m = 256^3 = 16,777,216, n = 256; 27-pt + 1e-2 I; Z ~ N(0,1) (34.4 GB) on the GPU."""
+CONFIG5_ZCHUNK = 16  # columns of Z drawn per seeded generator (config5_Z)
+
+
+def config5_Z(m, n, rows=None):
+    """Config-5 Z ~ N(0,1), m x n column-major on the GPU, drawn in blocks of
+    CONFIG5_ZCHUNK columns, block b from SeedSequence([1703, 10440, 5, 1, b]),
+    so any row range (one rank's rows) is reproducible without the whole
+    34 GB matrix on one device."""
     import torch
 
     dev = torch.device("cuda")
-    indptr, indices, data = stencil27_device(n_side, 1e-2, dev)
+    r0, r1 = rows if rows is not None else (0, m)
+    Zt = torch.empty((n, r1 - r0), dtype=torch.float64, device=dev)
+    for b, c0 in enumerate(range(0, n, CONFIG5_ZCHUNK)):
+        c1 = min(n, c0 + CONFIG5_ZCHUNK)
+        if rows is None:
+            torch.randn((c1 - c0, m), generator=_torch_gen(5, 1, dev, b), dtype=torch.float64,
+                        device=dev, out=Zt[c0:c1])
+        else:
+            blk = torch.randn((c1 - c0, m), generator=_torch_gen(5, 1, dev, b), dtype=torch.float64, device=dev)
+            Zt[c0:c1].copy_(blk[:, r0:r1])
+            del blk
+    return Zt.t()
+
+
+def config5(device=True, n_side=256, n=256, planes=None):
+    """m = 256^3 = 16,777,216, n = 256; 27-pt + 1e-2 I; Z ~ N(0,1) (34.4 GB) on the GPU.
+
+    ``planes = (z0, z1)``: only those grid planes' rows (row-partitioned runs)."""
+    import torch
+
+    dev = torch.device("cuda")
+    indptr, indices, data = stencil27_device(n_side, 1e-2, dev, planes)
     m = n_side ** 3
-    Z = torch.randn((n, m), generator=_torch_gen(5, 1, dev), dtype=torch.float64, device=dev).t()
+    z0, z1 = planes if planes is not None else (0, n_side)
+    Z = config5_Z(m, n, rows=(z0 * n_side * n_side, z1 * n_side * n_side) if planes is not None else None)
     return (indptr, indices, data), Z
 
 
