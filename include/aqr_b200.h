@@ -205,6 +205,28 @@ AQR_API aqr_status aqr_apply_block_dense(int64_t m, int64_t k, const double *A, 
 AQR_API aqr_status aqr_csr_matvec(int64_t m, const int32_t *indptr, const int32_t *indices,
                           const double *data, const double *x, double *y, void *stream);
 
+/* Dense helpers of the reference's kernel namespace, same operation order
+ * (_kernels_impl.py:59-82, 134-164), on caller-owned device buffers:
+ *   aqr_gemm_tn        C (p x n) = A^T B, A m x p, B m x n; every entry a
+ *                      sequential sum over ascending rows (gemm_tn; the
+ *                      Gram products of cholesky_qr and of the metrics)
+ *   aqr_gemm_nn        C (m x n) = A B, A m x kk; entry (i, j) accumulated
+ *                      over ascending l (gemm_nn / linalg.matmul)
+ *   aqr_cholesky_upper R = upper Cholesky factor of G (its upper triangle;
+ *                      linalg.cholesky_upper passes (G + G^T) / 2), left
+ *                      looking (cholesky_upper_kernel); *fail_dev (device
+ *                      int32) = -1, or the first failing pivot
+ *   aqr_tri_solve_right X with X R = Z (tri_solve_right_kernel); the caller
+ *                      checks that diag(R) is nonzero and finite (linalg.py). */
+AQR_API aqr_status aqr_gemm_tn(int64_t m, int64_t p, int64_t n, const double *A, int64_t lda, const double *B,
+                               int64_t ldb, double *C, int64_t ldc, void *stream);
+AQR_API aqr_status aqr_gemm_nn(int64_t m, int64_t kk, int64_t n, const double *A, int64_t lda, const double *B,
+                               int64_t ldb, double *C, int64_t ldc, void *stream);
+AQR_API aqr_status aqr_cholesky_upper(int64_t n, const double *G, int64_t ldg, double *R, int64_t ldr,
+                                      int32_t *fail_dev, void *stream);
+AQR_API aqr_status aqr_tri_solve_right(int64_t m, int64_t n, const double *Z, int64_t ldz, const double *R,
+                                       int64_t ldr, double *X, int64_t ldx, void *stream);
+
 /* ---- step kernels (one MGS step of the row-oriented fused schedule) ----
  * Used by the multi-GPU driver, which inserts its NCCL all-reduces between
  * *_partials and *_finish.  `ntiles` = aqr_num_tiles(m_local).

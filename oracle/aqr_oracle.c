@@ -34,7 +34,7 @@
 /* Tolerance calibration only: mode 1 swaps the
  * sequential dot for a pairwise one, the perturbation a GPU tree reduction
  * introduces.  Mode 0 (default) is the reference. */
-static int g_dot_mode = 0;
+static _Thread_local int g_dot_mode = 0; /* per thread: concurrent calibration runs */
 void aqro_set_dot_mode(int mode) { g_dot_mode = mode; }
 
 static double pairwise_dot(int64_t m, const double *x, const double *y) {
@@ -285,6 +285,77 @@ int64_t aqro_gs_factor(int family, int variant, int orientation, int64_t m, int6
     if (fail_val) *fail_val = s.fail_val;
     free(s.Zw); free(s.P); free(s.xbuf); free(s.Z0); free(s.X);
     return bad ? s.fail_col : -1;
+}
+
+/* ---- weighted Cholesky QR: gram_schmidt.py:209-218 ---------------- */
+
+/* cholesky_upper_kernel (_kernels_impl.py:134-152): left-looking, G's upper
+ * triangle as given, R zero-filled first.  Returns -1, or the failing pivot. */
+int64_t aqro_cholesky_upper_kernel(int64_t n, const double *G, double *R) {
+    memset(R, 0, (size_t)n * n * sizeof(double));
+    for (int64_t k = 0; k < n; ++k) {
+        double s = 0.0;
+        for (int64_t i = 0; i < k; ++i) s += R[i + k * n] * R[i + k * n];
+        const double t = G[k + k * n] - s;
+        if (!(t > 0.0) || !isfinite(t)) return k;
+        const double rkk = sqrt(t);
+        R[k + k * n] = rkk;
+        for (int64_t j = k + 1; j < n; ++j) {
+            s = 0.0;
+            for (int64_t i = 0; i < k; ++i) s += R[i + k * n] * R[i + j * n];
+            R[k + j * n] = (G[k + j * n] - s) / rkk;
+        }
+    }
+    return -1;
+}
+
+/* linalg.cholesky_upper (linalg.py:191-208): the kernel on (G + G^T) / 2 */
+static int64_t cholesky_upper(int64_t n, const double *G, double *R) {
+    double *Gs = (double *)malloc((size_t)n * n * sizeof(double));
+    if (!Gs) return -3;
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) Gs[i + j * n] = 0.5 * (G[i + j * n] + G[j + i * n]);
+    const int64_t bad = aqro_cholesky_upper_kernel(n, Gs, R);
+    free(Gs);
+    return bad;
+}
+
+/* linalg.tri_solve_right -> tri_solve_right_kernel (_kernels_impl.py:155-164) */
+void aqro_tri_solve_right_kernel(int64_t m, int64_t n, const double *Z, const double *R, double *X) {
+    for (int64_t k = 0; k < n; ++k) {
+        const double rkk = R[k + k * n];
+        for (int64_t r = 0; r < m; ++r) {
+            double s = 0.0;
+            for (int64_t i = 0; i < k; ++i) s += X[r + i * m] * R[i + k * n];
+            X[r + k * m] = (Z[r + k * m] - s) / rkk;
+        }
+    }
+}
+
+/* Returns -1 on success, the pivot (>= 0) on NotPositiveDefiniteError, -2 on
+ * a DimensionError, -3 on allocation failure, -4 on SingularMatrixError. */
+int64_t aqro_cholesky_qr(int64_t m, int64_t n, const double *Z, int op_kind, const double *A,
+                         const int64_t *indptr, const int64_t *indices, const double *data, double *Q,
+                         double *R, int64_t *mv_count) {
+    if (n < 1 || m < n) return -2;
+    aqro_op op = {op_kind, m, A, indptr, indices, data};
+    double *X = (double *)malloc((size_t)m * n * sizeof(double));
+    double *G = (double *)malloc((size_t)n * n * sizeof(double));
+    if (!X || !G) {
+        free(X); free(G);
+        return -3;
+    }
+    op_apply_block(&op, n, Z, X); /* X = op.apply_block(Z) */
+    if (mv_count) *mv_count = n;
+    aqro_gemm_tn(m, n, n, Z, X, G); /* G = matmul_tn(Z, X) */
+    int64_t bad = cholesky_upper(n, G, R);
+    if (bad == -1) {
+        for (int64_t k = 0; k < n; ++k)
+            if (R[k + k * n] == 0.0 || !isfinite(R[k + k * n])) bad = -4;
+        if (bad == -1) aqro_tri_solve_right_kernel(m, n, Z, R, Q);
+    }
+    free(X); free(G);
+    return bad;
 }
 
 /* ---- generator helpers (tests only) ---------------------------------- */

@@ -48,6 +48,15 @@ def lib():
                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                 _d, ctypes.c_int, _d, _i64, _i64, _d, _d, _d, _i32, _i64, _d,
             ]
+            L.aqro_cholesky_upper_kernel.restype = ctypes.c_int64
+            L.aqro_cholesky_upper_kernel.argtypes = [ctypes.c_int64, _d, _d]
+            L.aqro_tri_solve_right_kernel.restype = None
+            L.aqro_tri_solve_right_kernel.argtypes = [ctypes.c_int64, ctypes.c_int64, _d, _d, _d]
+            L.aqro_apply_block_dense.restype = None
+            L.aqro_apply_block_dense.argtypes = [ctypes.c_int64, ctypes.c_int64, _d, _d, _d]
+            L.aqro_cholesky_qr.restype = ctypes.c_int64
+            L.aqro_cholesky_qr.argtypes = [ctypes.c_int64, ctypes.c_int64, _d, ctypes.c_int, _d, _i64, _i64, _d,
+                                           _d, _d, _i64]
             L.aqro_last_phase_times.restype = None
             L.aqro_last_phase_times.argtypes = [_d]
             L.aqro_set_dot_mode.restype = None
@@ -87,7 +96,8 @@ class pairwise_dots:
 
     Used only to calibrate parity tolerances: the
     spread between the two orders is the rounding noise any reordered
-    (e.g. GPU tree) reduction is entitled to.  Not thread-safe.
+    (e.g. GPU tree) reduction is entitled to.  The mode is per thread (the
+    calling thread's oracle calls only).
     """
 
     def __enter__(self):
@@ -163,6 +173,45 @@ def extrapolate_seconds(phases, n_run, n_full):
     return (apply_s + norm_s) * lin + proj_s * pairs
 
 
+class OracleNotPositiveDefinite(Exception):
+    def __init__(self, pivot):
+        super().__init__(f"matrix not positive definite at pivot {pivot}")
+        self.pivot = pivot
+
+
+def _op_args(op):
+    null_d = ctypes.cast(None, _d)
+    null_i = ctypes.cast(None, _i64)
+    if op[0] == "dense":
+        A = np.asfortranarray(op[1], dtype=np.float64)
+        return (A,), (0, _p(A), null_i, null_i, null_d)
+    indptr = np.ascontiguousarray(op[1], dtype=np.int64)
+    indices = np.ascontiguousarray(op[2], dtype=np.int64)
+    data = np.ascontiguousarray(op[3], dtype=np.float64)
+    return (indptr, indices, data), (1, null_d, _p(indptr, _i64), _p(indices, _i64), _p(data))
+
+
+def cholesky_qr(Z, op):
+    """Weighted Cholesky QR (gram_schmidt.py:209-218); raises OracleNotPositiveDefinite."""
+    Z = np.asfortranarray(Z, dtype=np.float64)
+    m, n = Z.shape
+    Q = np.zeros((m, n), order="F")
+    R = np.zeros((n, n), order="F")
+    mv = ctypes.c_int64(0)
+    keep, args = _op_args(op)
+    rc = lib().aqro_cholesky_qr(m, n, _p(Z), *args, _p(Q), _p(R), ctypes.byref(mv))
+    del keep
+    if rc == -2:
+        raise ValueError(f"oracle: bad shape {Z.shape}")
+    if rc == -3:
+        raise MemoryError("oracle: allocation failed")
+    if rc == -4:
+        raise ZeroDivisionError("oracle: singular triangular factor")
+    if rc >= 0:
+        raise OracleNotPositiveDefinite(int(rc))
+    return OracleResult(Q, R, [], int(mv.value))
+
+
 def csr_matvec(indptr, indices, data, x):
     indptr = np.ascontiguousarray(indptr, dtype=np.int64)
     indices = np.ascontiguousarray(indices, dtype=np.int64)
@@ -197,6 +246,32 @@ def gemm_tn(A, B):
     C = np.empty((A.shape[1], B.shape[1]), order="F")
     lib().aqro_gemm_tn(A.shape[0], A.shape[1], B.shape[1], _p(A), _p(B), _p(C))
     return C
+
+
+def apply_block_dense(A, X):
+    """Y = A X, column c exactly like matvec (_kernels_impl.py:35-47)."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    X = np.asfortranarray(X, dtype=np.float64)
+    Y = np.empty((A.shape[0], X.shape[1]), order="F")
+    lib().aqro_apply_block_dense(A.shape[0], X.shape[1], _p(A), _p(X), _p(Y))
+    return Y
+
+
+def cholesky_upper_kernel(G):
+    """(pivot or -1, R): _kernels_impl.py:134-152 on G's upper triangle."""
+    G = np.asfortranarray(G, dtype=np.float64)
+    R = np.zeros_like(G, order="F")
+    bad = lib().aqro_cholesky_upper_kernel(G.shape[0], _p(G), _p(R))
+    return int(bad), R
+
+
+def tri_solve_right_kernel(Z, R):
+    """X with X R = Z (_kernels_impl.py:155-164)."""
+    Z = np.asfortranarray(Z, dtype=np.float64)
+    R = np.asfortranarray(R, dtype=np.float64)
+    X = np.empty_like(Z, order="F")
+    lib().aqro_tri_solve_right_kernel(Z.shape[0], Z.shape[1], _p(Z), _p(R), _p(X))
+    return X
 
 
 def householder_q(G):

@@ -96,6 +96,10 @@ SIGNATURES = {
     "aqr_matvec": (c_i32, [c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "aqr_apply_block_dense": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_csr_matvec": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "aqr_gemm_tn": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "aqr_gemm_nn": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "aqr_cholesky_upper": (c_i32, [c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_vp]),
+    "aqr_tri_solve_right": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_tile_rows": (c_i64, [c_i64]),
     "aqr_num_tiles": (c_i64, [c_i64]),
     "aqr_step_col_update_norm": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/aqr_b200.h"
+#include "aqr_dense.cuh"
 #include "aqr_kernels.cuh"
 #include "aqr_p2p.cuh"
 
@@ -1776,6 +1777,56 @@ aqr_status aqr_csr_matvec(int64_t m, const int32_t *indptr, const int32_t *indic
     op.indices = indices;
     op.data = data;
     return aqr_op_apply(&op, 1, x, m, y, m, stream);
+}
+
+// ---- dense helpers in the reference's order (aqr_dense.cuh) -----------------
+
+aqr_status aqr_gemm_tn(int64_t m, int64_t p, int64_t n, const double *A, int64_t lda, const double *B,
+                       int64_t ldb, double *C, int64_t ldc, void *stream) {
+    if (m < 0 || p < 0 || n < 0 || (m > 0 && (lda < m || ldb < m)) || ldc < std::max<int64_t>(p, 1))
+        return set_err(AQR_EARG, "gemm_tn: bad shape / leading dimension");
+    if (p == 0 || n == 0) return AQR_OK;
+    dim3 grid((unsigned)((p + aqr::kTnTile - 1) / aqr::kTnTile), (unsigned)((n + aqr::kTnTile - 1) / aqr::kTnTile));
+    aqr::gemm_tn_seq_kernel<<<grid, aqr::kBlock, 0, S(stream)>>>(m, p, n, A, lda, B, ldb, C, ldc);
+    return launched("gemm_tn_seq_kernel");
+}
+
+aqr_status aqr_gemm_nn(int64_t m, int64_t kk, int64_t n, const double *A, int64_t lda, const double *B,
+                       int64_t ldb, double *C, int64_t ldc, void *stream) {
+    if (m < 0 || kk < 0 || n < 0 || lda < std::max<int64_t>(m, 1) || ldb < std::max<int64_t>(kk, 1) ||
+        ldc < std::max<int64_t>(m, 1))
+        return set_err(AQR_EARG, "gemm_nn: bad shape / leading dimension");
+    if (m == 0 || n == 0) return AQR_OK;
+    if (kk == 0) {
+        AQR_CUDA(cudaMemset2DAsync(C, 8 * (size_t)ldc, 0, 8 * (size_t)m, (size_t)n, S(stream)));
+        return AQR_OK;
+    }
+    // C(:, j) accumulates exactly like matvec: the rectangular dense apply
+    aqr_op op;
+    std::memset(&op, 0, sizeof op);
+    op.kind = AQR_OP_DENSE;
+    op.m = m;
+    op.ncols = kk;
+    op.A = A;
+    op.lda = lda;
+    return dense_apply(&op, n, B, ldb, C, ldc, S(stream));
+}
+
+aqr_status aqr_cholesky_upper(int64_t n, const double *G, int64_t ldg, double *R, int64_t ldr, int32_t *fail_dev,
+                              void *stream) {
+    if (n < 1 || ldg < n || ldr < n || !G || !R || !fail_dev) return set_err(AQR_EARG, "cholesky_upper: bad arguments");
+    aqr::cholesky_upper_kernel<<<1, aqr::kBlock, 0, S(stream)>>>(n, G, ldg, R, ldr, fail_dev);
+    return launched("cholesky_upper_kernel");
+}
+
+aqr_status aqr_tri_solve_right(int64_t m, int64_t n, const double *Z, int64_t ldz, const double *R, int64_t ldr,
+                               double *X, int64_t ldx, void *stream) {
+    if (m < 0 || n < 1 || ldz < std::max<int64_t>(m, 1) || ldx < std::max<int64_t>(m, 1) || ldr < n)
+        return set_err(AQR_EARG, "tri_solve_right: bad shape / leading dimension");
+    if (m == 0) return AQR_OK;
+    const int64_t grid = std::min<int64_t>((m + aqr::kBlock - 1) / aqr::kBlock, (int64_t)sm_count() * 8);
+    aqr::tri_solve_right_kernel<<<(unsigned)grid, aqr::kBlock, 0, S(stream)>>>(m, n, Z, ldz, R, ldr, X, ldx);
+    return launched("tri_solve_right_kernel");
 }
 
 aqr_status aqr_step_col_update_norm(int64_t m, double *z, const double *qprev, double *x,

@@ -24,7 +24,7 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .exceptions import BreakdownError, DimensionError, NotPositiveDefiniteError
+from .exceptions import BreakdownError, DimensionError
 from .operators import CostReport, SpdOperator, as_matrix
 
 UNIT_ROUNDOFF = 2.0 ** -53
@@ -285,32 +285,25 @@ def cgs(Z, op, variant="naive", orientation="col"):
 def cholesky_qr(Z, op):
     """Weighted Cholesky QR: R from chol(Z.T A Z), Q = Z R^{-1} (n MV) (gram_schmidt.py:209-218).
 
-    X = A Z runs in the aqr block-apply kernel; the Gram product, the n x n
-    Cholesky and the triangular solve are plain cuBLAS/cuSOLVER calls.
+    X = A Z in the block-apply kernel, the Gram product Z^T X, the n x n
+    left-looking Cholesky and the triangular solve in the repo's kernels in
+    the reference's operation order (linalg.py), so Q and R are bitwise the
+    reference's.
     """
+    from . import linalg
+
     Z, m, n = _check_inputs(Z, op)
     t = D.torch()
     back = _result_converter(Z)
     mv_before = op.mv_count
     Zd, _ = D.to_device_f(Z)
-    X = op.apply_block(Zd)
-    X = t.as_tensor(X, device=Zd.device)
-    G = Zd.transpose(0, 1) @ X
-    Gs = 0.5 * (G + G.transpose(0, 1))
-    Lc, info = t.linalg.cholesky_ex(Gs)
-    info = int(info)
-    if info > 0:
-        raise NotPositiveDefiniteError(info - 1)
-    Rd = Lc.transpose(0, 1).contiguous()
-    if not bool(t.isfinite(t.diagonal(Rd)).all()) or bool((t.diagonal(Rd) == 0).any()):
-        raise NotPositiveDefiniteError(int(t.nonzero(~(t.diagonal(Rd) > 0))[0]))
-    Qd = t.linalg.solve_triangular(Rd, Zd, upper=True, left=False)
-    R = D.empty_f(n, n)
-    R.copy_(Rd)
-    Qf = D.empty_f(m, n)
-    Qf.copy_(Qd)
+    X = t.as_tensor(op.apply_block(Zd), device=Zd.device)
+    G = linalg.matmul_tn(Zd, X)
+    del X
+    R = linalg.cholesky_upper(G)
+    Q = linalg.tri_solve_right(Zd, R)
     cost = CostReport(op.mv_count - mv_before, _model_flops("cholqr", None, m, n))
-    return QrResult(back(Qf), back(R), cost)
+    return QrResult(back(Q), back(R), cost)
 
 
 def _check_orientation(orientation):

@@ -42,3 +42,29 @@ def spread(Z, spec, method):
 def tolerance(Z, spec, method):
     sq, sr = spread(Z, spec, method)
     return max(TOL_FACTOR * sq, FLOOR), max(TOL_FACTOR * sr, FLOOR)
+
+
+def calibrated(Z, spec, methods, threads=None):
+    """{method: (oracle result, q tolerance, r tolerance)} for one input.
+
+    Runs the oracle with sequential dots (the reference) and with pairwise
+    dots (the calibration) for every method concurrently on host threads
+    (the C oracle releases the GIL; the dot mode is per thread)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def seq(meth):
+        return O.gs_factor(Z, spec, meth)
+
+    def pw(meth):
+        with O.pairwise_dots():
+            return O.gs_factor(Z, spec, meth)
+
+    jobs = [(meth, fn) for meth in methods for fn in (seq, pw)]
+    with ThreadPoolExecutor(threads or len(jobs)) as ex:
+        futs = {(meth, fn.__name__): ex.submit(fn, meth) for meth, fn in jobs}
+    out = {}
+    for meth in methods:
+        s, p = futs[(meth, "seq")].result(), futs[(meth, "pw")].result()
+        sq, sr = factor_errors(p.Q, p.R, s.Q, s.R)
+        out[meth] = (s, max(TOL_FACTOR * sq, FLOOR), max(TOL_FACTOR * sr, FLOOR))
+    return out

@@ -94,3 +94,37 @@ def test_cfg1_inputs_and_outputs_pinned(golden_cases, golden):
         assert np.array_equal(r.R, golden[f"cfg1|{meth}|R"])
         assert r.flagged_columns == ref["flagged"]
         assert r.mv_count == ref["mv_count"]
+
+
+@pytest.mark.parametrize("key", ["hand", "dense0", "dense1", "dense2", "dense3", "dense7"])
+def test_oracle_cholqr_bitwise_equals_reference(golden, key):
+    # gram_schmidt.py:209-218 with linalg.cholesky_upper / tri_solve_right
+    r = O.cholesky_qr(golden[f"{key}|Z"], _op(golden, key))
+    assert np.array_equal(r.Q, golden[f"{key}|cholqr|Q"])
+    assert np.array_equal(r.R, golden[f"{key}|cholqr|R"])
+    assert r.mv_count == int(golden[f"{key}|cholqr|mv"][0])
+
+
+def test_oracle_cholqr_not_positive_definite():
+    # rank-deficient Z: the Gram matrix is singular, the pivot fails
+    Z = np.array([[1.0, 2.0], [0.0, 0.0], [0.0, 0.0]])
+    with pytest.raises(O.OracleNotPositiveDefinite) as info:
+        O.cholesky_qr(Z, ("dense", np.eye(3)))
+    assert info.value.pivot == 1
+
+
+def test_oracle_pairwise_mode_is_per_thread():
+    # the calibration mode is thread-local: concurrent runs do not see it
+    import threading
+
+    rng = np.random.default_rng(5)
+    x, y = rng.standard_normal(10001), rng.standard_normal(10001)
+    seq = O.seq_dot(x, y)
+    out = {}
+    with O.pairwise_dots():
+        t = threading.Thread(target=lambda: out.setdefault("v", O.seq_dot(x, y)))
+        t.start()
+        t.join()
+        pw = O.seq_dot(x, y)
+    assert out["v"] == seq
+    assert pw != seq or True  # pairwise may coincide; the other thread must not switch
