@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define AQR_ABI_VERSION 1
+#define AQR_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define AQR_API __attribute__((visibility("default")))
@@ -55,7 +55,9 @@ typedef enum {
     AQR_ECUDA = 3,      /* CUDA runtime / launch failure                       */
     AQR_EARG = 4,       /* bad enum, null pointer, size out of range           */
     AQR_ENOMEM = 5,     /* workspace too small / device allocation failed      */
-    AQR_ECALLBACK = 6   /* a user operator callback returned non-zero          */
+    AQR_ECALLBACK = 6,  /* a user operator callback returned non-zero          */
+    AQR_ETIMEOUT = 7    /* multi-GPU: a peer's exchange flag did not arrive in
+                           time (the group must be re-created on every rank) */
 } aqr_status;
 
 typedef enum { AQR_MGS = 0, AQR_CGS = 1 } aqr_family;           /* MethodId.family  */
@@ -298,6 +300,7 @@ typedef struct aqr_p2p_group {
     int64_t n_halo;
     const int32_t *halo_rank, *halo_row; /* device */
     uint64_t seq0; /* flag epoch: advance by n + 2 per factorization, same on all ranks */
+    uint64_t timeout_ns; /* longest wait for one peer flag (0: 60 s), then AQR_ETIMEOUT */
 } aqr_p2p_group;
 
 /* Bytes of one rank's exchange buffer for n columns. */

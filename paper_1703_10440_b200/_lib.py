@@ -13,9 +13,9 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # AQR_LIB_PATH: an alternative build of the same library (tools/ A/B experiments)
 LIB_PATH = os.environ.get("AQR_LIB_PATH") or os.path.join(_HERE, "libaqr_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
-AQR_OK, AQR_EDIM, AQR_EBREAKDOWN, AQR_ECUDA, AQR_EARG, AQR_ENOMEM, AQR_ECALLBACK = range(7)
+AQR_OK, AQR_EDIM, AQR_EBREAKDOWN, AQR_ECUDA, AQR_EARG, AQR_ENOMEM, AQR_ECALLBACK, AQR_ETIMEOUT = range(8)
 AQR_MGS, AQR_CGS = 0, 1
 AQR_NAIVE, AQR_HA, AQR_HP = 0, 1, 2
 AQR_COL, AQR_ROW = 0, 1
@@ -65,7 +65,7 @@ class AqrP2PGroup(ctypes.Structure):
         ("nranks", c_i32), ("rank", c_i32),
         ("xbuf", c_vp * MAX_RANKS), ("W", c_vp * MAX_RANKS), ("ldw", c_i64 * MAX_RANKS),
         ("n_halo", c_i64), ("halo_rank", c_vp), ("halo_row", c_vp),
-        ("seq0", c_u64),
+        ("seq0", c_u64), ("timeout_ns", c_u64),
     ]
 
 

@@ -1503,6 +1503,8 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
     P.m_loc = m;
     P.halo_rank = g->halo_rank;
     P.halo_row = g->halo_row;
+    P.status = status;
+    P.timeout_ns = g->timeout_ns ? g->timeout_ns : 60ull * 1000000000ull;
 
     if (a->Z != a->Q) AQR_CUDA(copy_cols(a->Q, a->ldq, a->Z, a->ldz, m, n, cudaMemcpyDeviceToDevice, s));
     AQR_TRY(aqr_status_init(status, n, stream));
@@ -1612,6 +1614,7 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
     AQR_CUDA(cudaMemcpyAsync(st.data(), status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
     AQR_CUDA(cudaStreamSynchronize(s));
     a->mv_count = mv;
+    if (st[1] == 1) return set_err(AQR_ETIMEOUT, "peer exchange timed out (a rank is missing or failed)");
     if (a->flagged_host) std::memcpy(a->flagged_host, st.data() + 4, 4 * n);
     if (st[0] >= 0) {
         a->fail_col = st[0];

@@ -59,6 +59,8 @@ struct P2PArgs {
     int64_t m_loc;
     const int32_t *halo_rank;  // extended column m_loc + h lives on rank halo_rank[h] ...
     const int32_t *halo_row;   // ... at its local row halo_row[h]
+    int32_t *status;           // this rank's status block (timeout record: [1] = 1)
+    uint64_t timeout_ns;       // longest wait for one flag
 };
 
 __device__ __forceinline__ uint64_t *xb_flag(double *xb, int64_t n, int kind, int src) {
@@ -80,12 +82,34 @@ __device__ __forceinline__ void publish(const P2PArgs &p, int kind, uint64_t v) 
     for (int r = 0; r < p.nranks; ++r) flag_release(xb_flag(p.xb[r], p.n, kind, p.rank), v);
 }
 
-// One thread: wait until every rank raised `kind` to at least v.
-__device__ __forceinline__ void wait_all(const P2PArgs &p, int kind, uint64_t v) {
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// One thread: wait until every rank raised `kind` to at least v.  Bounded:
+// a wait longer than p.timeout_ns (a peer died or was never launched)
+// records the timeout in the status block -- [1] = 1 and [0] set, so every
+// later kernel of this rank returns at its status check -- and gives up;
+// it also gives up as soon as the status block records a failure.  Returns
+// false when it gave up.
+__device__ __forceinline__ bool wait_all(const P2PArgs &p, int kind, uint64_t v) {
+    const uint64_t t0 = global_ns();
     for (int src = 0; src < p.nranks; ++src) {
         const uint64_t *f = xb_flag(p.xb[p.rank], p.n, kind, src);
-        while (flag_acquire(f) < v) __nanosleep(100);
+        while (flag_acquire(f) < v) {
+            if (failed(p.status)) return false;
+            if (global_ns() - t0 > p.timeout_ns) {
+                atomicExch(p.status + 1, 1);
+                atomicCAS(p.status, -1, 0x7fffffff);
+                __threadfence_system();
+                return false;
+            }
+            __nanosleep(200);
+        }
     }
+    return true;
 }
 
 __device__ __forceinline__ uint64_t seq_step(const P2PArgs &p, int64_t i) { return p.seq0 + 1 + (uint64_t)i; }
@@ -294,8 +318,8 @@ __global__ void __launch_bounds__(kBlock) p2p_trailing_kernel(TrailArgs a, P2PAr
     extern __shared__ double wsum[];
     __shared__ double rii_sh;
     __shared__ int ok_sh;
-    if (threadIdx.x == 0) {
-        wait_all(p, kFlagNorm, seq_step(p, i));
+    if (threadIdx.x == 0) ok_sh = 0;
+    if (threadIdx.x == 0 && wait_all(p, kFlagNorm, seq_step(p, i))) {
         const int par = (int)(i & 1);
         const double t = sum_ranks(p, xb_norm(p.n, par, 0) + 0, 4);
         const double zz = sum_ranks(p, xb_norm(p.n, par, 0) + 1, 4);

@@ -23,6 +23,13 @@ from .gram_schmidt import QrResult, _model_flops
 from .operators import CostReport
 
 
+class PeerExchangeTimeout(RuntimeError):
+    """A peer's exchange flag did not arrive within the group's timeout.
+
+    Every rank that sees it drops its peer group; the next call re-creates it
+    collectively (new buffers, flags from zero)."""
+
+
 def _dist():
     import torch.distributed as dist
 
@@ -32,7 +39,7 @@ def _dist():
 class PeerGroup:
     """This rank's W (m_loc x n) and exchange buffer, plus every peer's mapping."""
 
-    def __init__(self, m_loc, n, group=None):
+    def __init__(self, m_loc, n, group=None, timeout_s=60.0):
         dist = _dist()
         self.L = L = _lib.lib()
         self.group = group
@@ -60,6 +67,7 @@ class PeerGroup:
             else:
                 w, x = self._open(h_w), self._open(h_x)
             self.desc.W[r], self.desc.xbuf[r], self.desc.ldw[r] = w, x, max(int(m_r), 1)
+        self.desc.timeout_ns = int(timeout_s * 1e9)
         self.next_seq = 1
 
     def _alloc(self, nbytes):
@@ -98,8 +106,12 @@ def supported(op, method):
             and method.variant in ("ha", "hp") and method.family in ("mgs", "cgs"))
 
 
-def p2p_factorize(Z_local, op, method, group=None):
-    """Row-partitioned factorization over peer memory (every rank calls it)."""
+def p2p_factorize(Z_local, op, method, group=None, timeout_s=60.0):
+    """Row-partitioned factorization over peer memory (every rank calls it).
+
+    A rank that waits longer than ``timeout_s`` for a peer's exchange flag
+    raises PeerExchangeTimeout (the kernels give up instead of spinning
+    forever)."""
     t = D.torch()
     L = _lib.lib()
     m_loc, n = (int(s) for s in Z_local.shape)
@@ -110,10 +122,11 @@ def p2p_factorize(Z_local, op, method, group=None):
     key = (m_loc, n, id(group))
     pg = getattr(op, "_peer_groups", {}).get(key)
     if pg is None:
-        pg = PeerGroup(m_loc, n, group)
+        pg = PeerGroup(m_loc, n, group, timeout_s)
         op._peer_groups = {**getattr(op, "_peer_groups", {}), key: pg}
     if not hasattr(op, "_halo_dev"):
         op._halo_dev = (t.from_numpy(op.halo_rank).to(D.device()), t.from_numpy(op.halo_row).to(D.device()))
+    pg.desc.timeout_ns = int(timeout_s * 1e9)
     hr, hw = op._halo_dev
     pg.desc.n_halo = int(hr.numel())
     pg.desc.halo_rank = hr.data_ptr() if hr.numel() else None
@@ -139,6 +152,10 @@ def p2p_factorize(Z_local, op, method, group=None):
     a.flagged_host = flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
     mv_before = op.mv_count
     status = L.aqr_p2p_gs_factor(ctypes.byref(a), ctypes.byref(pg.desc), D.stream_ptr())
+    if status == _lib.AQR_ETIMEOUT:
+        op._peer_groups = {k: v for k, v in op._peer_groups.items() if v is not pg}
+        pg.close()
+        raise PeerExchangeTimeout(L.aqr_last_error().decode())
     if status == _lib.AQR_EBREAKDOWN:
         f = int(a.fail_col)
         op.mv_count += n if method.variant == "hp" else f + 1

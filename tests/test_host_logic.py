@@ -153,9 +153,11 @@ def test_ctypes_struct_layout_matches_header():
     # aqr_op / aqr_factor_args as declared in include/aqr_b200.h (LP64)
     assert ctypes.sizeof(_lib.AqrOp) == 4 + 4 + 8 + 8 + 8 + 8 * 3 + 8 + 8 * 3 + 8
     assert _lib.AqrFactorArgs.flagged_host.offset == 4 * 4 + 8 * 2 + 8 * 6 + 8 + 8 + 8 + 8 + 8 + 8
-    # aqr_p2p_group: 2 x int32, 3 arrays of AQR_MAX_RANKS (8) pointers / int64, n_halo, 2 pointers, seq0
-    assert ctypes.sizeof(_lib.AqrP2PGroup) == 8 + 3 * 8 * 8 + 8 + 16 + 8
+    # aqr_p2p_group: 2 x int32, 3 arrays of AQR_MAX_RANKS (8) pointers / int64, n_halo, 2 pointers,
+    # seq0, timeout_ns
+    assert ctypes.sizeof(_lib.AqrP2PGroup) == 8 + 3 * 8 * 8 + 8 + 16 + 8 + 8
     assert _lib.AqrP2PGroup.seq0.offset == 8 + 3 * 64 + 8 + 16
+    assert _lib.AqrP2PGroup.timeout_ns.offset == 8 + 3 * 64 + 8 + 16 + 8
 
 
 def test_generators_match_reference_laplacian(golden):
