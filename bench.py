@@ -528,10 +528,14 @@ def run_b200_distributed(args, rank, world, local_rank):
 
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        # the peer-memory kernels of different ranks wait on each other's
+        # flags: ranks sharing a GPU are not guaranteed to run concurrently
+        # (tests/test_gpu_multirank.py emulates N ranks on one device instead)
+        raise SystemExit(f"{world} ranks need {world} GPUs, this node has {torch.cuda.device_count()}")
     # the step loop has no collective call (peer-memory flags); the process
     # group only bootstraps (IPC handles, halo plan) and takes the max over
-    # ranks, so gloo is enough -- and it also runs ranks that share a device
-    # (one leased GPU under MPS: NCCL refuses duplicate GPUs)
+    # ranks, so gloo is enough
     dist.init_process_group("gloo", rank=rank, world_size=world)
     L = _lib.lib()
     wl = device_workload(5, rank, world)

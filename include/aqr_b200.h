@@ -318,6 +318,18 @@ AQR_API aqr_status aqr_ipc_close(void *ptr);
  * Collective: every rank calls it with the same n, method and seq0. */
 AQR_API aqr_status aqr_p2p_gs_factor(aqr_factor_args *args, const aqr_p2p_group *group, void *stream);
 
+/* Single-device emulation of an N-rank group (tests; one GPU standing in for
+ * N): args[r] / groups[r] describe rank r (all W / exchange buffers on the
+ * current device, plain pointers instead of IPC mappings).  The ranks'
+ * launches are interleaved phase by phase on `stream` -- step i's norm
+ * kernels of all ranks, then their trailing passes, then their R-row pushes
+ * -- so every flag a kernel waits for was raised by a kernel that precedes
+ * it in stream order: the same kernels, flags, halo reads and rank-ordered
+ * sums as N processes, without kernels that wait on one another running
+ * concurrently on one GPU.  Returns the first non-OK rank status. */
+AQR_API aqr_status aqr_p2p_gs_factor_lockstep(int32_t nranks, aqr_factor_args *const *args,
+                                              const aqr_p2p_group *const *groups, void *stream);
+
 /* ---- instrumentation (bench.py) ------------------------------------------
  * aqr_launch_count: number of kernels this library has launched so far in
  * the process (monotonic; read before/after a timed region).

@@ -81,6 +81,8 @@ SIGNATURES = {
     "aqr_ipc_open": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_vp)]),
     "aqr_ipc_close": (c_i32, [c_vp]),
     "aqr_p2p_gs_factor": (c_i32, [ctypes.POINTER(AqrFactorArgs), ctypes.POINTER(AqrP2PGroup), c_vp]),
+    "aqr_p2p_gs_factor_lockstep": (c_i32, [c_i32, ctypes.POINTER(ctypes.POINTER(AqrFactorArgs)),
+                                           ctypes.POINTER(ctypes.POINTER(AqrP2PGroup)), c_vp]),
     "aqr_trace_read": (c_i64, [c_vp, c_i64]),
     "aqr_gs_factor_d2h": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_gs_factor_pinned": (c_i32, [ctypes.POINTER(AqrFactorArgs), c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,

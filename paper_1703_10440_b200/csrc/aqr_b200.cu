@@ -1456,73 +1456,112 @@ aqr_status aqr_ipc_close(void *ptr) {
     return AQR_OK;
 }
 
-aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *stream) {
-    if (!a || !g) return set_err(AQR_EARG, "null args");
-    a->fail_col = -1;
-    a->fail_val = 0.0;
-    a->mv_count = 0;
-    const int64_t m = a->m, n = a->n;
-    if (g->nranks < 1 || g->nranks > aqr::kMaxRanks || g->rank < 0 || g->rank >= g->nranks)
-        return set_err(AQR_EARG, "bad group");
-    if (a->orientation != AQR_ROW || (a->variant != AQR_HA && a->variant != AQR_HP) || a->family < 0 ||
-        a->family > 1)
-        return set_err(AQR_EARG, "peer-memory path: row orientation, HA or HP");
-    if (!a->op || a->op->kind != AQR_OP_CSR || a->op->m != m)
-        return set_err(AQR_EARG, "peer-memory path: local CSR operator with m = local rows");
-    if (n < 1 || m < 1) return set_err(AQR_EDIM, "empty local block");
-    if (a->Q != g->W[g->rank] || a->ldq != g->ldw[g->rank] || a->ldq < m || !a->Z || a->ldz < m || !a->R ||
-        a->ldr < n)
-        return set_err(AQR_EARG, "Q must be the group's working matrix of this rank");
-    if (g->n_halo > 0 && (!g->halo_rank || !g->halo_row)) return set_err(AQR_EARG, "halo tables missing");
-    const Layout L = layout(a->family, a->variant, AQR_ROW, m, n);
-    if (!a->workspace || a->workspace_bytes < L.total)
-        return set_err(AQR_ENOMEM, "workspace smaller than aqr_workspace_bytes()");
-    const bool hp = a->variant == AQR_HP, cgs = a->family == AQR_CGS;
-    cudaStream_t s = S(stream);
-    void *ws = a->workspace;
-    int32_t *status = at<int32_t>(ws, L.status);
-    unsigned *counters = at<unsigned>(ws, L.counters);
-    double *Rt = at<double>(ws, L.rt), *partial = at<double>(ws, L.partial), *npart = at<double>(ws, L.npart);
-    double *xvec = at<double>(ws, L.xvec), *zvec = at<double>(ws, L.zvec), *pring = at<double>(ws, L.pring);
-    double *X = at<double>(ws, L.X), *Z0 = at<double>(ws, L.Z0);
-    double *W = a->Q;
-    const int64_t ldw = a->ldq;
-    auto col = [&](double *B, int64_t ld, int64_t j) { return B + j * ld; };
+}  // extern "C"
 
+namespace {
+
+// One rank's peer-memory factorization, split into the phases of the step
+// loop so that the single-rank driver (aqr_p2p_gs_factor) runs them in order
+// and the lock-step emulation (aqr_p2p_gs_factor_lockstep) interleaves the
+// ranks phase by phase on one stream.
+struct P2PRun {
+    aqr_factor_args *a = nullptr;
+    const aqr_p2p_group *g = nullptr;
+    cudaStream_t s = nullptr;
+    int64_t m = 0, n = 0, ldw = 0, mv = 0;
+    bool hp = false, cgs = false;
+    int32_t *status = nullptr;
+    unsigned *counters = nullptr;
+    double *Rt = nullptr, *partial = nullptr, *npart = nullptr, *xvec = nullptr, *zvec = nullptr,
+           *pring = nullptr, *X = nullptr, *Z0 = nullptr, *W = nullptr;
+    int32_t ntiles = 0;
     aqr::P2PArgs P;
-    std::memset(&P, 0, sizeof P);
-    P.nranks = g->nranks;
-    P.rank = g->rank;
-    for (int r = 0; r < g->nranks; ++r) {
-        P.xb[r] = g->xbuf[r];
-        P.W[r] = g->W[r];
-        P.ldw[r] = g->ldw[r];
-    }
-    P.n = n;
-    P.seq0 = g->seq0;
-    P.m_loc = m;
-    P.halo_rank = g->halo_rank;
-    P.halo_row = g->halo_row;
-    P.status = status;
-    P.timeout_ns = g->timeout_ns ? g->timeout_ns : 60ull * 1000000000ull;
-
-    if (a->Z != a->Q) AQR_CUDA(copy_cols(a->Q, a->ldq, a->Z, a->ldz, m, n, cudaMemcpyDeviceToDevice, s));
-    AQR_TRY(aqr_status_init(status, n, stream));
-    AQR_CUDA(cudaMemsetAsync(counters, 0, 4 * (size_t)(n + 8), s));
-    AQR_CUDA(cudaMemsetAsync(Rt, 0, 8 * (size_t)n * n, s));
-    if (cgs) AQR_CUDA(copy_cols(Z0, m, a->Q, a->ldq, m, n, cudaMemcpyDeviceToDevice, s));
-    aqr::p2p_barrier_kernel<<<1, 1, 0, s>>>(P);  // this rank's Z is in place
-    AQR_TRY(launched("p2p_barrier_kernel"));
-    const aqr_op *op = a->op;
     aqr::CsrArgs c;
-    std::memset(&c, 0, sizeof c);
-    c.m = m;
-    c.indptr = op->indptr;
-    c.indices = op->indices;
-    c.data = op->data;
-    c.trace = -1;
-    int64_t mv = 0;
-    if (hp) {  // X = op.apply_block(Zw), halo columns from the owners
+    std::vector<int32_t> st;
+
+    double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
+
+    aqr_status init(aqr_factor_args *args, const aqr_p2p_group *grp, cudaStream_t stream) {
+        a = args;
+        g = grp;
+        s = stream;
+        if (!a || !g) return set_err(AQR_EARG, "null args");
+        a->fail_col = -1;
+        a->fail_val = 0.0;
+        a->mv_count = 0;
+        m = a->m;
+        n = a->n;
+        if (g->nranks < 1 || g->nranks > aqr::kMaxRanks || g->rank < 0 || g->rank >= g->nranks)
+            return set_err(AQR_EARG, "bad group");
+        if (a->orientation != AQR_ROW || (a->variant != AQR_HA && a->variant != AQR_HP) || a->family < 0 ||
+            a->family > 1)
+            return set_err(AQR_EARG, "peer-memory path: row orientation, HA or HP");
+        if (!a->op || a->op->kind != AQR_OP_CSR || a->op->m != m)
+            return set_err(AQR_EARG, "peer-memory path: local CSR operator with m = local rows");
+        if (n < 1 || m < 1) return set_err(AQR_EDIM, "empty local block");
+        if (a->Q != g->W[g->rank] || a->ldq != g->ldw[g->rank] || a->ldq < m || !a->Z || a->ldz < m || !a->R ||
+            a->ldr < n)
+            return set_err(AQR_EARG, "Q must be the group's working matrix of this rank");
+        if (g->n_halo > 0 && (!g->halo_rank || !g->halo_row)) return set_err(AQR_EARG, "halo tables missing");
+        const Layout L = layout(a->family, a->variant, AQR_ROW, m, n);
+        if (!a->workspace || a->workspace_bytes < L.total)
+            return set_err(AQR_ENOMEM, "workspace smaller than aqr_workspace_bytes()");
+        hp = a->variant == AQR_HP;
+        cgs = a->family == AQR_CGS;
+        void *ws = a->workspace;
+        status = at<int32_t>(ws, L.status);
+        counters = at<unsigned>(ws, L.counters);
+        Rt = at<double>(ws, L.rt);
+        partial = at<double>(ws, L.partial);
+        npart = at<double>(ws, L.npart);
+        xvec = at<double>(ws, L.xvec);
+        zvec = at<double>(ws, L.zvec);
+        pring = at<double>(ws, L.pring);
+        X = at<double>(ws, L.X);
+        Z0 = at<double>(ws, L.Z0);
+        W = a->Q;
+        ldw = a->ldq;
+        ntiles = (int32_t)aqr::num_tiles(m);
+        std::memset(&P, 0, sizeof P);
+        P.nranks = g->nranks;
+        P.rank = g->rank;
+        for (int r = 0; r < g->nranks; ++r) {
+            P.xb[r] = g->xbuf[r];
+            P.W[r] = g->W[r];
+            P.ldw[r] = g->ldw[r];
+        }
+        P.n = n;
+        P.seq0 = g->seq0;
+        P.m_loc = m;
+        P.halo_rank = g->halo_rank;
+        P.halo_row = g->halo_row;
+        P.status = status;
+        P.timeout_ns = g->timeout_ns ? g->timeout_ns : 60ull * 1000000000ull;
+        const aqr_op *op = a->op;
+        std::memset(&c, 0, sizeof c);
+        c.m = m;
+        c.indptr = op->indptr;
+        c.indices = op->indices;
+        c.data = op->data;
+        c.trace = -1;
+        return AQR_OK;
+    }
+
+    // Z into W, the status block, the start barrier (this rank's Z is in place).
+    aqr_status begin() {
+        if (a->Z != a->Q) AQR_CUDA(copy_cols(a->Q, a->ldq, a->Z, a->ldz, m, n, cudaMemcpyDeviceToDevice, s));
+        AQR_TRY(aqr_status_init(status, n, s));
+        AQR_CUDA(cudaMemsetAsync(counters, 0, 4 * (size_t)(n + 8), s));
+        AQR_CUDA(cudaMemsetAsync(Rt, 0, 8 * (size_t)n * n, s));
+        if (cgs) AQR_CUDA(copy_cols(Z0, m, a->Q, a->ldq, m, n, cudaMemcpyDeviceToDevice, s));
+        aqr::p2p_barrier_kernel<<<1, 1, 0, s>>>(P);
+        return launched("p2p_barrier_kernel");
+    }
+
+    // HP: X = op.apply_block(Zw) (line 136), halo columns from the owners
+    // (waits for every rank's start barrier).
+    aqr_status block_apply() {
+        if (!hp) return AQR_OK;
         aqr::CsrArgs b = c;
         b.k = n;
         b.X = W;
@@ -1533,9 +1572,12 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
         aqr::p2p_csr_block_kernel<<<(unsigned)std::min<int64_t>(nb, (int64_t)sm_count() * 8), aqr::kBlock, 0, s>>>(b, P);
         AQR_TRY(launched("p2p_csr_block_kernel"));
         mv += n;
+        return AQR_OK;
     }
-    const int32_t ntiles = (int32_t)aqr::num_tiles(m);
-    for (int64_t i = 0; i < n; ++i) {
+
+    // Step i, first launch: r_{i-1,i} from the exchanged R rows, the deferred
+    // column update (+ SpMV for HA), the norm partials -> every rank.
+    aqr_status norm(int64_t i) {
         aqr::NormOut o;
         std::memset(&o, 0, sizeof o);
         o.npart = npart;
@@ -1555,24 +1597,27 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
             ca.out = o;
             ca.trace = -1;
             launch_pdl(aqr::p2p_col_update_kernel, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
-            AQR_TRY(launched("p2p_col_update_kernel"));
-        } else {
-            aqr::CsrArgs ca = c;
-            ca.k = 1;
-            ca.X = col(W, ldw, i);
-            ca.ldx = m;
-            ca.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
-            ca.Y = xvec;
-            ca.ldy = m;
-            ca.znew = zvec;
-            ca.out = o;
-            if (op->max_row_nnz >= 1 && op->max_row_nnz <= 5)
-                launch_pdl(aqr::p2p_csr_step_kernel<5>, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
-            else
-                launch_pdl(aqr::p2p_csr_step_kernel<8>, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
-            AQR_TRY(launched("p2p_csr_step_kernel"));
-            ++mv;
+            return launched("p2p_col_update_kernel");
         }
+        aqr::CsrArgs ca = c;
+        ca.k = 1;
+        ca.X = col(W, ldw, i);
+        ca.ldx = m;
+        ca.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+        ca.Y = xvec;
+        ca.ldy = m;
+        ca.znew = zvec;
+        ca.out = o;
+        if (a->op->max_row_nnz >= 1 && a->op->max_row_nnz <= 5)
+            launch_pdl(aqr::p2p_csr_step_kernel<5>, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
+        else
+            launch_pdl(aqr::p2p_csr_step_kernel<8>, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
+        ++mv;
+        return launched("p2p_csr_step_kernel");
+    }
+
+    // Step i, second launch: r_ii from every rank's norm totals, the trailing pass.
+    aqr_status trail(int64_t i) {
         aqr::TrailArgs t;
         std::memset(&t, 0, sizeof t);
         t.m = m;
@@ -1596,32 +1641,88 @@ aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *s
         t.status = status;
         t.trace = -1;
         t.reverse = (int32_t)(i & 1);  // backwards on odd steps (L2 reuse, as the single-GPU pass)
-        aqr_status st;
-        if (hp) st = cgs ? launch_p2p_trailing<true, true>(t, P, i, Rt + i * n + i, status, s)
-                         : launch_p2p_trailing<true, false>(t, P, i, Rt + i * n + i, status, s);
-        else st = cgs ? launch_p2p_trailing<false, true>(t, P, i, Rt + i * n + i, status, s)
-                      : launch_p2p_trailing<false, false>(t, P, i, Rt + i * n + i, status, s);
-        AQR_TRY(st);
-        if (i + 1 < n) {
-            launch_pdl(aqr::p2p_rrow_kernel, (unsigned)(n - 1 - i), aqr::kBlock, 0, s, (const double *)partial,
-                       (int32_t)ntiles, (int64_t)(i + 1), P, (int64_t)i, counters + 1, (const int32_t *)status);
-            AQR_TRY(launched("p2p_rrow_kernel"));
+        double *rii = Rt + i * n + i;
+        if (hp) return cgs ? launch_p2p_trailing<true, true>(t, P, i, rii, status, s)
+                           : launch_p2p_trailing<true, false>(t, P, i, rii, status, s);
+        return cgs ? launch_p2p_trailing<false, true>(t, P, i, rii, status, s)
+                   : launch_p2p_trailing<false, false>(t, P, i, rii, status, s);
+    }
+
+    // Step i, third launch: this rank's R-row totals -> every rank.
+    aqr_status rrow(int64_t i) {
+        if (i + 1 >= n) return AQR_OK;
+        launch_pdl(aqr::p2p_rrow_kernel, (unsigned)(n - 1 - i), aqr::kBlock, 0, s, (const double *)partial,
+                   (int32_t)ntiles, (int64_t)(i + 1), P, (int64_t)i, counters + 1, (const int32_t *)status);
+        return launched("p2p_rrow_kernel");
+    }
+
+    aqr_status end() {
+        aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, Rt, a->R, a->ldr);
+        AQR_TRY(launched("finalize_r_kernel"));
+        st.assign((16 + 4 * n) / 4, 0);
+        AQR_CUDA(cudaMemcpyAsync(st.data(), status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
+        return AQR_OK;
+    }
+
+    // After the stream drained: the status record -> return code / outputs.
+    aqr_status finish() {
+        a->mv_count = mv;
+        if (st[1] == 1) return set_err(AQR_ETIMEOUT, "peer exchange timed out (a rank is missing or failed)");
+        if (a->flagged_host) std::memcpy(a->flagged_host, st.data() + 4, 4 * n);
+        if (st[0] >= 0) {
+            a->fail_col = st[0];
+            std::memcpy(&a->fail_val, st.data() + 2, 8);
+            return set_err(AQR_EBREAKDOWN, "breakdown at column " + std::to_string(st[0]));
         }
+        return AQR_OK;
     }
-    aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, Rt, a->R, a->ldr);
-    AQR_TRY(launched("finalize_r_kernel"));
-    std::vector<int32_t> st((16 + 4 * n) / 4);
-    AQR_CUDA(cudaMemcpyAsync(st.data(), status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
-    AQR_CUDA(cudaStreamSynchronize(s));
-    a->mv_count = mv;
-    if (st[1] == 1) return set_err(AQR_ETIMEOUT, "peer exchange timed out (a rank is missing or failed)");
-    if (a->flagged_host) std::memcpy(a->flagged_host, st.data() + 4, 4 * n);
-    if (st[0] >= 0) {
-        a->fail_col = st[0];
-        std::memcpy(&a->fail_val, st.data() + 2, 8);
-        return set_err(AQR_EBREAKDOWN, "breakdown at column " + std::to_string(st[0]));
+};
+
+}  // namespace
+
+extern "C" {
+
+aqr_status aqr_p2p_gs_factor(aqr_factor_args *a, const aqr_p2p_group *g, void *stream) {
+    P2PRun r;
+    AQR_TRY(r.init(a, g, S(stream)));
+    AQR_TRY(r.begin());
+    AQR_TRY(r.block_apply());
+    for (int64_t i = 0; i < r.n; ++i) {
+        AQR_TRY(r.norm(i));
+        AQR_TRY(r.trail(i));
+        AQR_TRY(r.rrow(i));
     }
-    return AQR_OK;
+    AQR_TRY(r.end());
+    AQR_CUDA(cudaStreamSynchronize(r.s));
+    return r.finish();
+}
+
+aqr_status aqr_p2p_gs_factor_lockstep(int32_t nranks, aqr_factor_args *const *args,
+                                      const aqr_p2p_group *const *groups, void *stream) {
+    if (nranks < 1 || nranks > aqr::kMaxRanks || !args || !groups) return set_err(AQR_EARG, "bad rank list");
+    std::vector<P2PRun> runs((size_t)nranks);
+    for (int r = 0; r < nranks; ++r) {
+        AQR_TRY(runs[r].init(args[r], groups[r], S(stream)));
+        if (groups[r]->rank != r || groups[r]->nranks != nranks || runs[r].n != runs[0].n)
+            return set_err(AQR_EARG, "lock-step ranks must be 0..nranks-1 of one group, same n");
+    }
+    // every phase of every rank is enqueued only after the phases it waits
+    // for (stream order), so no kernel ever spins on a flag not yet raised
+    for (auto &r : runs) AQR_TRY(r.begin());
+    for (auto &r : runs) AQR_TRY(r.block_apply());
+    for (int64_t i = 0; i < runs[0].n; ++i) {
+        for (auto &r : runs) AQR_TRY(r.norm(i));
+        for (auto &r : runs) AQR_TRY(r.trail(i));
+        for (auto &r : runs) AQR_TRY(r.rrow(i));
+    }
+    for (auto &r : runs) AQR_TRY(r.end());
+    AQR_CUDA(cudaStreamSynchronize(S(stream)));
+    aqr_status first = AQR_OK;
+    for (auto &r : runs) {
+        const aqr_status st = r.finish();
+        if (first == AQR_OK) first = st;
+    }
+    return first;
 }
 
 aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientation, int64_t m,

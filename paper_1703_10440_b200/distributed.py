@@ -58,6 +58,15 @@ def row_partition(m, world, align=1):
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
 
+def _halo_need(indices, r0, r1, owner):
+    """{owner rank: ascending global columns outside [r0, r1) that the block reads}."""
+    ext = np.unique(indices[(indices < r0) | (indices >= r1)])
+    need = {}
+    for c in ext.tolist():
+        need.setdefault(owner(c), []).append(c)
+    return need
+
+
 class DistCsrSpdOperator(SpdOperator):
     """The local row block of a row-partitioned CSR operator.
 
@@ -71,7 +80,7 @@ class DistCsrSpdOperator(SpdOperator):
     """
 
     def __init__(self, indptr, indices, data, partition, rank, group=None, local_apply=None,
-                 device=None):
+                 device=None, needs=None):
         self.partition = [tuple(p) for p in partition]
         self.rank = rank
         self.group = group
@@ -92,15 +101,14 @@ class DistCsrSpdOperator(SpdOperator):
         def owner(c):
             return bisect.bisect_right(starts, c) - 1
 
-        ext = np.unique(indices[(indices < r0) | (indices >= r1)])
-        need = {}
-        for c in ext.tolist():
-            need.setdefault(owner(c), []).append(c)
-        # every rank learns who needs which of its rows (one collective, once)
-        dist = _dist()
+        need = _halo_need(indices, r0, r1, owner)
         world = len(self.partition)
-        gathered = [None] * world
-        dist.all_gather_object(gathered, need, group=group)
+        if needs is None:
+            # every rank learns who needs which of its rows (one collective, once)
+            gathered = [None] * world
+            _dist().all_gather_object(gathered, need, group=group)
+        else:  # every rank's halo plan given (single-process emulation, blocks_of)
+            gathered = list(needs)
         self.send = {}  # peer -> local row offsets to send
         for peer in range(world):
             if peer == rank:
@@ -132,6 +140,22 @@ class DistCsrSpdOperator(SpdOperator):
         self.indptr, self.indices_local, self.data = indptr, local, data
         self._dev = None
         self._desc = None
+
+    @classmethod
+    def blocks_of(cls, indptr, indices, data, partition):
+        """Every rank's block of a global CSR matrix, built in one process
+        without a process group (the single-device lock-step emulation,
+        p2p.p2p_factorize_lockstep)."""
+        indptr = np.asarray(indptr, dtype=np.int64)
+        indices = np.asarray(indices, dtype=np.int64)
+        starts = [p[0] for p in partition]
+
+        def owner(c):
+            return bisect.bisect_right(starts, c) - 1
+
+        needs = [_halo_need(indices[indptr[r0]:indptr[r1]], r0, r1, owner) for r0, r1 in partition]
+        return [cls(indptr[r0:r1 + 1] - indptr[r0], indices[indptr[r0]:indptr[r1]], data[indptr[r0]:indptr[r1]],
+                    partition, rank, needs=needs) for rank, (r0, r1) in enumerate(partition)]
 
     @property
     def nnz(self):

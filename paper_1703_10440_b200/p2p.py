@@ -165,3 +165,116 @@ def p2p_factorize(Z_local, op, method, group=None, timeout_s=60.0):
     Q = W.clone()  # W is this group's working matrix, reused by the next call
     cost = CostReport(op.mv_count - mv_before, _model_flops(method.family, method.variant, op.global_dim, n))
     return QrResult(Q, R, cost, [int(j) for j in np.flatnonzero(flags)])
+
+
+class _EmulatedGroup:
+    """Rank ``rank`` of a single-device emulated group: plain device pointers
+    to every rank's W / exchange buffer (no IPC)."""
+
+    def __init__(self, L, rank, ws, xbs, m_locs, n, timeout_s):
+        self.W, self.xb = ws[rank], xbs[rank]
+        self.m_loc, self.n = m_locs[rank], n
+        self.desc = _lib.AqrP2PGroup()
+        self.desc.nranks, self.desc.rank = len(ws), rank
+        for r in range(len(ws)):
+            self.desc.W[r], self.desc.xbuf[r], self.desc.ldw[r] = ws[r], xbs[r], max(int(m_locs[r]), 1)
+        self.desc.timeout_ns = int(timeout_s * 1e9)
+
+    def W_tensor(self):
+        return D.wrap(self.W, self.m_loc, self.n, max(self.m_loc, 1))
+
+
+def p2p_factorize_lockstep(Z_blocks, ops, method, seq0=1, timeout_s=60.0, solo=None):
+    """Run an N-rank peer-memory factorization on ONE device (tests).
+
+    ``Z_blocks[r]`` / ``ops[r]`` are rank r's row block and local operator
+    (``DistCsrSpdOperator.blocks_of``).  The library interleaves the ranks'
+    launches phase by phase on the current stream
+    (``aqr_p2p_gs_factor_lockstep``), so every flag a kernel waits for is
+    already raised when it starts -- the multi-rank kernels, flags, halo
+    reads and rank-ordered sums run without kernels that wait on one another
+    sharing the GPU.  Returns one QrResult per rank (Q = the rank's rows).
+
+    ``solo=r`` launches rank r alone (the others never start): its waits
+    must end in PeerExchangeTimeout after ``timeout_s`` (bounded-wait test;
+    one kernel waits, nothing else needs to run beside it)."""
+    from .gram_schmidt import MethodId
+
+    t = D.torch()
+    L = _lib.lib()
+    if not isinstance(method, MethodId):
+        method = MethodId.parse(method)
+    N = len(ops)
+    n = int(Z_blocks[0].shape[1])
+    m_locs = [int(Zb.shape[0]) for Zb in Z_blocks]
+    own = []
+
+    def alloc(nbytes):
+        p = ctypes.c_void_p()
+        _lib.check(L.aqr_p2p_alloc(nbytes, ctypes.byref(p)), "aqr_p2p_alloc")
+        own.append(p.value)
+        return p.value
+
+    try:
+        ws = [alloc(8 * max(m, 1) * n) for m in m_locs]
+        xbs = [alloc(int(L.aqr_p2p_exchange_bytes(n))) for _ in range(N)]
+        groups, argv, keep = [], [], []
+        fam, var = _lib.FAMILY_CODE[method.family], _lib.VARIANT_CODE[method.variant]
+        for r in range(N):
+            g = _EmulatedGroup(L, r, ws, xbs, m_locs, n, timeout_s)
+            op = ops[r]
+            hr = t.from_numpy(op.halo_rank).to(D.device())
+            hw = t.from_numpy(op.halo_row).to(D.device())
+            g.desc.n_halo = int(hr.numel())
+            g.desc.halo_rank = hr.data_ptr() if hr.numel() else None
+            g.desc.halo_row = hw.data_ptr() if hw.numel() else None
+            g.desc.seq0 = seq0
+            Zd, ldz = D.to_device_f(Z_blocks[r])
+            R = D.empty_f(n, n)
+            wsb = t.empty(int(L.aqr_workspace_bytes(fam, var, _lib.ORIENTATION_CODE["row"], m_locs[r], n)),
+                          dtype=t.uint8, device=R.device)
+            flags = np.zeros(n, dtype=np.int32)
+            a = _lib.AqrFactorArgs()
+            a.family, a.variant, a.orientation = fam, var, _lib.ORIENTATION_CODE["row"]
+            a.m, a.n = m_locs[r], n
+            a.Z, a.ldz = Zd.data_ptr(), ldz
+            a.Q, a.ldq = g.W, max(m_locs[r], 1)
+            a.R, a.ldr = R.data_ptr(), n
+            a.op = ctypes.pointer(op._native())
+            a.workspace, a.workspace_bytes = wsb.data_ptr(), wsb.numel()
+            a.flagged_host = flags.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            groups.append(g)
+            argv.append(a)
+            keep.append((hr, hw, Zd, R, wsb, flags))
+        arr_a = (ctypes.POINTER(_lib.AqrFactorArgs) * N)(*[ctypes.pointer(a) for a in argv])
+        arr_g = (ctypes.POINTER(_lib.AqrP2PGroup) * N)(*[ctypes.pointer(g.desc) for g in groups])
+        if solo is not None:
+            status = L.aqr_p2p_gs_factor(ctypes.pointer(argv[solo]), ctypes.pointer(groups[solo].desc),
+                                         D.stream_ptr())
+        else:
+            status = L.aqr_p2p_gs_factor_lockstep(N, arr_a, arr_g, D.stream_ptr())
+        if status == _lib.AQR_ETIMEOUT:
+            raise PeerExchangeTimeout(L.aqr_last_error().decode())
+        if solo is not None:
+            raise RuntimeError(f"a solo rank finished with status {status}")
+        if status == _lib.AQR_EBREAKDOWN:
+            cols = {(int(a.fail_col), float(a.fail_val)) for a in argv}
+            if len(cols) != 1:
+                raise RuntimeError(f"ranks disagree on the breakdown: {sorted(cols)}")
+            f = int(argv[0].fail_col)
+            for r in range(N):
+                ops[r].mv_count += n if method.variant == "hp" else f + 1
+            raise BreakdownError(f, float(argv[0].fail_val))
+        _lib.check(status, "aqr_p2p_gs_factor_lockstep")
+        out = []
+        for r in range(N):
+            ops[r].mv_count += n
+            Q = groups[r].W_tensor().clone()
+            cost = CostReport(n, _model_flops(method.family, method.variant, ops[r].global_dim, n))
+            out.append(QrResult(Q, keep[r][3], cost, [int(j) for j in np.flatnonzero(keep[r][5])]))
+        D.torch().cuda.current_stream().synchronize()
+        return out
+    finally:
+        D.torch().cuda.synchronize()
+        for p in own:
+            L.aqr_p2p_free(p)
