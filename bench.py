@@ -111,12 +111,17 @@ def config_dict(cfg, method, m, n, nnz, world):
     return d
 
 
-def step_bytes(variant, m, n, bytes_A):
-    """Algorithmic HBM bytes of one factorization (one-pass look-ahead model)."""
+def step_bytes(variant, m, n, bytes_A, lazy_x=True):
+    """Algorithmic HBM bytes of one factorization (one-pass look-ahead model).
+
+    HP with ``lazy_x`` (the single-GPU row form): X = A Z is never rewritten;
+    step j forms x_j from X_j and the j finished p columns (col_lazy_norm_kernel),
+    so the X term is sum_j 8 m j = T / 2 instead of SURVEY 8d's second T
+    (``lazy_x=False``: the eager model, which the peer-memory path still runs)."""
     T = 8 * m * n * (n - 1)
     mv = bytes_A + 16 * m
     return {"ha": T + n * mv + 32 * m * n, "naive": T + 2 * n * mv + 32 * m * n,
-            "hp": 2 * T + (bytes_A + 16 * m * n) + 32 * m * n}[variant]
+            "hp": (T + T // 2 if lazy_x else 2 * T) + (bytes_A + 16 * m * n) + 32 * m * n}[variant]
 
 
 def measured_peaks():
@@ -424,6 +429,10 @@ def run_b200(args, rank, world, local_rank):
     sb = step_bytes(variant, m, n, bytes_A)
     step_gbs = sb / (ms_per_step / 1e3) / 1e9
     roofline["step"] = {"achieved": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": sb}
+    if variant == "hp":  # what the eager schedule would have to move in the same time
+        eager = step_bytes(variant, m, n, bytes_A, lazy_x=False)
+        roofline["step"]["survey_8d_bytes"] = eager
+        roofline["step"]["survey_8d_equivalent_gbs"] = eager / (ms_per_step / 1e3) / 1e9
 
     # ---- end to end: numpy Z in, numpy Q / R out, through the public API ----
     e2e = None
@@ -580,7 +589,7 @@ def run_b200_distributed(args, rank, world, local_rank):
     gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
     dist.all_gather(gathered, per_rank)
     bytes_A = 12 * 449_455_096 + 4 * (m + 1)
-    sb = step_bytes("hp", m, n, bytes_A)
+    sb = step_bytes("hp", m, n, bytes_A, lazy_x=False)
     step_gbs = sb / (ms_per_step / 1e3) / 1e9
     e2e = None
     if not args.no_e2e:

@@ -12,6 +12,10 @@ SOURCES = [os.path.join(HERE, "csrc", "aqr_b200.cu")]
 DEPENDS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [
     os.path.join(REPO, "include", "aqr_b200.h")]
 OUT = os.path.join(HERE, "libaqr_b200.so")
+# The experiments build: the same library with the A/B knobs read from the
+# environment (-DAQR_EXPERIMENTS; the shipped OUT ignores them).  Loaded via
+# AQR_LIB_PATH by tests/test_gpu_variants.py and the tools/ab_*.sh scripts.
+OUT_EXP = os.path.join(HERE, "libaqr_b200_exp.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -50,5 +54,14 @@ def build(force=False, verbose=False, out=None, defines=()):
     return target
 
 
+def build_experiments(force=False, verbose=False):
+    if not force and os.path.exists(OUT_EXP) and all(os.path.getmtime(p) <= os.path.getmtime(OUT_EXP)
+                                                    for p in DEPENDS):
+        return OUT_EXP
+    return build(out=OUT_EXP, defines=("AQR_EXPERIMENTS",), verbose=verbose)
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--experiments" in sys.argv:
+        print(build_experiments(force="--force" in sys.argv, verbose="-v" in sys.argv))

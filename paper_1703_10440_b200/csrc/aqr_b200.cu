@@ -142,25 +142,56 @@ void timer_end(long idx, cudaStream_t s) {
     cudaEventRecord(g_timer.recs[(size_t)idx].e1, s);
 }
 
-// Experiment knob (read once): AQR_TRAIL_VARIANT (see launch_trailing).
-int trail_variant() {
-    static const int v = [] {
-        const char *e = std::getenv("AQR_TRAIL_VARIANT");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
+// Experiment knobs.  The A/B measurements behind the design (tools/ab_*.sh,
+// DESIGN.md) select alternative schedules through environment variables --
+// but only in the experiments build (-DAQR_EXPERIMENTS,
+// libaqr_b200_exp.so, _build.build_experiments()).  The shipped library
+// compiles every knob to its default: no environment variable changes what
+// it runs.
+int knob(const char *name, int dflt) {
+#ifdef AQR_EXPERIMENTS
+    const char *e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
 }
+#define AQR_KNOB(fn, name, dflt)                   \
+    int fn() {                                     \
+        static const int v = knob(name, dflt);     \
+        return v;                                  \
+    }
 
-// Experiment knob (read once): AQR_CARVEOUT = -1 leaves the driver's choice,
-// otherwise the preferred shared-memory carveout (percent) of the per-step
-// kernels, so consecutive launches need no L1/shared reconfiguration.
-int carveout_pct() {
-    static const int v = [] {
-        const char *e = std::getenv("AQR_CARVEOUT");
-        return e ? std::atoi(e) : -1;
-    }();
-    return v;
-}
+// AQR_CARVEOUT = -1 leaves the driver's choice, otherwise the preferred
+// shared-memory carveout (percent) of the per-step kernels.
+AQR_KNOB(carveout_pct, "AQR_CARVEOUT", -1)
+// AQR_PDL=0: no programmatic dependent launch for the per-step kernels.
+AQR_KNOB(pdl_mode, "AQR_PDL", 1)
+// AQR_LDG_REVERSE=0: the trailing kernel always walks forwards.
+AQR_KNOB(ldg_reverse_mode, "AQR_LDG_REVERSE", 1)
+// AQR_TRAIL_VARIANT: columns per iteration of the trailing kernel (0 = the
+// default: 2 for MGS / CGS-HP, 1 for MGS-HP; 3 = 4 columns, 5 = 1 column,
+// 6 = HP with 2 columns).
+#ifdef AQR_EXPERIMENTS
+AQR_KNOB(trail_variant, "AQR_TRAIL_VARIANT", 0)
+#endif
+// AQR_SPMV_VARIANT=3: the unpipelined fused SpMV step.
+AQR_KNOB(spmv_variant, "AQR_SPMV_VARIANT", 0)
+// AQR_PLAIN_PF=0: plain SpMV on csr_row_kernel.
+AQR_KNOB(plain_pf_mode, "AQR_PLAIN_PF", 1)
+// AQR_TRAIL_CTAS: CTAs per SM the column grouping aims at.
+AQR_KNOB(trail_ctas_knob, "AQR_TRAIL_CTAS", 3)
+// AQR_COL_SCHEDULE=1: the column-oriented loop for the col methods.
+AQR_KNOB(col_schedule_mode, "AQR_COL_SCHEDULE", 0)
+// AQR_DIRECT=0: copy Z into Q first instead of reading Z in place.
+AQR_KNOB(direct_mode, "AQR_DIRECT", 1)
+// AQR_DEFER=0: a separate r-row reduction launch per step.
+AQR_KNOB(defer_mode, "AQR_DEFER", 1)
+// AQR_SPMV_REPEAT=k: k idempotent repeats of every fused SpMV step (diagnostics).
+AQR_KNOB(spmv_repeat, "AQR_SPMV_REPEAT", 0)
+// AQR_DEBUG_TIMING=1: host-side enqueue timings on stderr.
+AQR_KNOB(debug_timing, "AQR_DEBUG_TIMING", 0)
 
 template <typename K>
 void ensure_carveout(K kernel) {
@@ -176,24 +207,6 @@ void ensure_carveout(K kernel) {
         if (e.first == key && e.second == dev) return;
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     done.push_back({key, dev});
-}
-
-// Programmatic dependent launch for the per-step kernels (AQR_PDL=0 disables).
-int pdl_mode() {
-    static const int v = [] {
-        const char *e = std::getenv("AQR_PDL");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
-
-// AQR_LDG_REVERSE=0: the LDG trailing kernel always walks forwards (A/B).
-int ldg_reverse_mode() {
-    static const int v = [] {
-        const char *e = std::getenv("AQR_LDG_REVERSE");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
 }
 
 template <typename... KArgs, typename... Args>
@@ -270,10 +283,7 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
     if (out.npart != nullptr) {
         const int64_t nt = aqr::norm_tiles(op->m, false);
         const long tix = timer_begin(1, (double)op->m * 40.0 + (double)op->nnz * 12.0, s);
-        static const int sv = [] {
-            const char *e = std::getenv("AQR_SPMV_VARIANT");
-            return e ? std::atoi(e) : 0;
-        }();
+        const int sv = spmv_variant();
         const unsigned g1 = (unsigned)nt;  // the canonical norm grid (HA / naive)
         // software-pipelined fused step; row batch B = the longest row when
         // known and <= 8 (all of a row's loads in one batch, no predicated-off
@@ -297,10 +307,7 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         return launched("csr_step_kernel");
     }
     const int32_t mr = op->max_row_nnz;
-    static const int plain_pf = [] {  // AQR_PLAIN_PF=0: plain SpMV on csr_row_kernel (A/B)
-        const char *e = std::getenv("AQR_PLAIN_PF");
-        return e ? std::atoi(e) : 1;
-    }();
+    const int plain_pf = plain_pf_mode();
     if (k == 1 && mr >= 1 && mr <= 8 && plain_pf != 0 && AQR_SPMV_PF2 != 0) {
         // plain y = A x through the pipelined step kernel (no norms, no
         // update): rows three deep instead of one dependent chain per row
@@ -351,21 +358,7 @@ aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx
         aqr::dense_gemv_kernel<<<grid, aqr::kGemvBlock, 0, s>>>(m, ncols, op->A, op->lda, X, ldx, Y, ldy);
         return launched("dense_gemv_kernel");
     }
-    static const int gv = [] {  // AQR_GEMM_VARIANT=1: the 64 x 64 / 4 x 4 kernel (A/B)
-        const char *e = std::getenv("AQR_GEMM_VARIANT");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (gv == 1) {
-        dim3 grid((unsigned)((m + aqr::kGemmBM - 1) / aqr::kGemmBM),
-                  (unsigned)((k + aqr::kGemmBN - 1) / aqr::kGemmBN));
-        aqr::dense_gemm_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
-        return launched("dense_gemm_kernel");
-    }
     dim3 grid((unsigned)((m + aqr::kG2BM - 1) / aqr::kG2BM), (unsigned)((k + aqr::kG2BN - 1) / aqr::kG2BN));
-    if (gv == 2) {
-        aqr::dense_gemm2_kernel<<<grid, 256, 0, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
-        return launched("dense_gemm2_kernel");
-    }
     AQR_TRY(ensure_smem(aqr::dense_gemm3_kernel, aqr::kG3Smem));
     aqr::dense_gemm3_kernel<<<grid, 256, aqr::kG3Smem, s>>>(m, ncols, k, op->A, op->lda, X, ldx, Y, ldy);
     return launched("dense_gemm3_kernel");
@@ -431,6 +424,40 @@ aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, dou
     return launched("col_update_norm_kernel");
 }
 
+// HP row form, step j: x_j = X_j - sum_{k<j} r_{k,j} p_k, the deferred z_j
+// update and the norm partials (col_lazy_norm_kernel).
+aqr_status launch_col_lazy_norm(int64_t m, int64_t j, double *z, const double *zsrc, const double *qprev,
+                                const double *Xj, const double *P, int64_t ldp, const double *rcol,
+                                int64_t rstride, const double *r, double *xout, const aqr::NormOut &out,
+                                const aqr::RrowIn *rin, cudaStream_t s) {
+    aqr::ColArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.trace = trace_slot();
+    if (rin) a.rin = *rin;
+    a.m = m;
+    a.z = z;
+    a.zsrc = zsrc;
+    a.qprev = qprev;
+    a.x = const_cast<double *>(Xj);
+    a.r = r;
+    a.out = out;
+    a.out.ntiles = (int32_t)aqr::norm_tiles(m, true);
+    a.P = P;
+    a.ldp = ldp;
+    a.rcol = rcol;
+    a.rstride = rstride;
+    a.nprev = (int32_t)j;
+    a.xout = xout;
+    const int64_t nt = aqr::norm_tiles(m, true);
+    if (nt == 0) return AQR_OK;
+    ensure_carveout(aqr::col_lazy_norm_kernel);
+    // bytes: p_0..p_{j-1}, X_j, z_j (+ q_{j-1} and the z_j store), x_j store
+    const long tix = timer_begin(2, (double)m * (8.0 * (double)j + 8.0 + 8.0 + (j > 0 ? 16.0 : 0.0) + 8.0), s);
+    launch_pdl(aqr::col_lazy_norm_kernel, (unsigned)nt, aqr::kBlock, 0, s, a);
+    timer_end(tix, s);
+    return launched("col_lazy_norm_kernel");
+}
+
 // Algorithmic HBM bytes of one trailing launch: every trailing element read
 // once (and written once when the deferred update applies), the step's
 // vectors once.  Re-reads caused by column grouping are not counted.
@@ -450,13 +477,7 @@ constexpr int kMaxCpg = 256;
 // 2 (512 tiles) one group per tile -- each CTA walks all t columns and reads
 // the step vectors once -- beat two groups by 2.8 % (HA 7.51 -> 7.30 ms) and
 // 2 % (HP 12.59 -> 12.34 ms); 2 and 3 give the same grouping there.
-int trail_ctas_per_sm() {
-    static const int v = [] {
-        const char *e = std::getenv("AQR_TRAIL_CTAS");
-        return e ? std::max(1, std::atoi(e)) : 3;
-    }();
-    return v;
-}
+int trail_ctas_per_sm() { return std::max(1, trail_ctas_knob()); }
 
 int choose_cpg_generic(int64_t ntiles, int64_t ncols) {
     if (ncols <= 0) return 1;
@@ -476,82 +497,53 @@ aqr_status launch_rrow_reduce(int64_t m, int64_t ncols, const double *partial, d
 aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStream_t s,
                            bool *deferred = nullptr) {
     if (deferred) *deferred = false;
-    const int32_t tslot = trace_slot();
     aqr::TrailArgs a = a0;
-    a.trace = tslot;
+    a.trace = trace_slot();
     const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
     if (a.ntiles == 0) return AQR_OK;
     const bool big = aqr::rows_per_thread(a.m) == 8;
-    const bool aligned = (a.ldw % 2 == 0) && (!hp || a.ldx % 2 == 0) && (!cgs || a.ldz0 % 2 == 0) &&
-                         ((uintptr_t)a.W % 16 == 0) && (!hp || (uintptr_t)a.X % 16 == 0) &&
-                         (!cgs || (uintptr_t)a.Z0 % 16 == 0);
-    // Measured on B200 (tools/kernel_ab.py, config 2): the short-lived LDG
-    // kernel plus a separate totals launch beats the persistent TMA-pipelined
-    // kernel for HA (8.84 vs 9.26 ms/factorization) and HP (14.1 vs 14.4 ms).
-    // AQR_TRAIL_VARIANT: 0 = LDG, CU=2 (HA) / CU=1 (HP) (default), 3 = LDG CU=4 (HA),
-    // 5 = LDG CU=1 (HA), 6 = LDG CU=2 (HP),
-    // 1 = TMA without the L2 hint, 4 = TMA with the evict-first hint.
-    const int tv = trail_variant();
-    const bool tma = big && aligned && ncols <= aqr::kTmaMaxCols && (tv == 1 || tv == 4) && a.Wsrc == nullptr;
-    a.cpg = tma ? (int32_t)std::max<int64_t>(ncols, 1) : choose_cpg_generic(a.ntiles, ncols);
+    // A persistent TMA-bulk (cp.async.bulk + mbarrier, warp-specialized)
+    // form of this pass measured slower than this short-lived LDG kernel with
+    // deferred totals (HA 9.26 vs 8.84 ms, HP 14.4 vs 14.1 ms on config 2;
+    // DESIGN.md section 3) and was removed.
+    a.cpg = choose_cpg_generic(a.ntiles, ncols);
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
+    if (ldg_reverse_mode() == 0) a.reverse = 0;
 
     const long tix = timer_begin(0, trailing_bytes(a, hp, cgs), s);
-    if (tma) {
-        const int64_t units = (int64_t)a.ntiles * std::max<int64_t>(ncols, 1);
-#define TMA_LAUNCH(HP, CGS)                                                                      \
-    do {                                                                                         \
-        constexpr size_t smem = aqr::TmaCfg<HP, CGS>::kSmem;                                     \
-        AQR_TRY(ensure_smem(aqr::trailing_tma_kernel<HP, CGS, true>, smem));                     \
-        ensure_carveout(aqr::trailing_tma_kernel<HP, CGS, true>);                                \
-        ensure_carveout(aqr::trailing_tma_kernel<HP, CGS, false>);                               \
-        AQR_TRY(ensure_smem(aqr::trailing_tma_kernel<HP, CGS, false>, smem));                    \
-        /* all CTAs must be co-resident: the last ones wait for the grid */                     \
-        static int occ[64] = {0};                                                                \
-        int dev_ = 0;                                                                            \
-        cudaGetDevice(&dev_);                                                                    \
-        if (occ[dev_ & 63] == 0) {                                                               \
-            int o_ = 0;                                                                          \
-            AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                              \
-                &o_, aqr::trailing_tma_kernel<HP, CGS, true>, aqr::kTmaThreads, smem));          \
-            occ[dev_ & 63] = std::max(1, std::min(o_, 2));                                       \
-        }                                                                                        \
-        const unsigned grid = (unsigned)std::min<int64_t>(units, (int64_t)sm_count() * occ[dev_ & 63]); \
-        if (tv == 1)                                                                             \
-            launch_pdl(aqr::trailing_tma_kernel<HP, CGS, false>, grid, aqr::kTmaThreads, smem, s, a); \
-        else                                                                                     \
-            launch_pdl(aqr::trailing_tma_kernel<HP, CGS, true>, grid, aqr::kTmaThreads, smem, s, a); \
-    } while (0)
-        if (hp) { if (cgs) TMA_LAUNCH(true, true); else TMA_LAUNCH(true, false); }
-        else    { if (cgs) TMA_LAUNCH(false, true); else TMA_LAUNCH(false, false); }
-#undef TMA_LAUNCH
-    } else {
-        if (ldg_reverse_mode() == 0) a.reverse = 0;
-        dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
-        const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
-#define LAUNCH(RPT, CU, HP, CGS)                                                   \
-    do {                                                                           \
-        AQR_TRY(ensure_smem(aqr::trailing_kernel<RPT, CU, HP, CGS>, smem));        \
+    dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
+    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
+#define LAUNCH(RPT, CU, HP, CGS)                                                           \
+    do {                                                                                   \
+        AQR_TRY(ensure_smem(aqr::trailing_kernel<RPT, CU, HP, CGS>, smem));                \
         launch_pdl(aqr::trailing_kernel<RPT, CU, HP, CGS>, grid, aqr::kBlock, smem, s, a); \
     } while (0)
-        if (big) {
-            // MGS-HP: one column per iteration (128 registers, 2 CTAs/SM) measured
-            // 2.8 % faster than two (164 registers, 1 CTA/SM) on config 2;
-            // CGS-HP (144 registers either way: 1 CTA/SM) keeps two (12 % faster)
-            if (hp && (cgs || tv == 6)) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 2, true, false); }
-            else if (hp) LAUNCH(8, 1, true, false);
-            else if (tv == 5) { if (cgs) LAUNCH(8, 1, false, true); else LAUNCH(8, 1, false, false); }
-            else if (tv == 3) { if (cgs) LAUNCH(8, 4, false, true); else LAUNCH(8, 4, false, false); }
-            else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
-        } else {
-            if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
-            else    { if (cgs) LAUNCH(1, 4, false, true); else LAUNCH(1, 4, false, false); }
-        }
-#undef LAUNCH
+    if (big) {
+#ifdef AQR_EXPERIMENTS
+        // AQR_TRAIL_VARIANT: 3 = four columns per iteration, 5 = one, 6 = HP with two
+        const int tv = trail_variant();
+        if (tv == 6 && hp && !cgs) { LAUNCH(8, 2, true, false); goto done; }
+        if (tv == 5 && !hp) { if (cgs) LAUNCH(8, 1, false, true); else LAUNCH(8, 1, false, false); goto done; }
+        if (tv == 3 && !hp) { if (cgs) LAUNCH(8, 4, false, true); else LAUNCH(8, 4, false, false); goto done; }
+#endif
+        // Z-only passes (HA, naive and the lazy-x HP row form): two columns per
+        // iteration (120 registers, 2 CTAs/SM).  Passes that also carry X (the
+        // HP column loop): MGS one column per iteration (128 registers, 2
+        // CTAs/SM: 2.8 % faster than two at 164 registers / 1 CTA/SM on
+        // config 2), CGS two (144 registers either way; 12 % faster).
+        if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 1, true, false); }
+        else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
+    } else {
+        if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
+        else    { if (cgs) LAUNCH(1, 4, false, true); else LAUNCH(1, 4, false, false); }
     }
+#undef LAUNCH
+#ifdef AQR_EXPERIMENTS
+done:
+#endif
     timer_end(tix, s);
     AQR_TRY(launched("trailing_kernel"));
-    if (!tma && a.counters != nullptr && ncols > 0) {  // generic kernel: totals pending
+    if (a.counters != nullptr && ncols > 0) {  // totals pending
         if (deferred) {
             *deferred = true;
             return AQR_OK;
@@ -609,30 +601,6 @@ aqr_status side_acquire(SideCtx &c) {
 void side_release(const SideCtx &c) {
     std::lock_guard<std::mutex> lk(g_side_mu);
     g_side_free.push_back(c);
-}
-
-int col_schedule_mode() {  // AQR_COL_SCHEDULE=1: the column-oriented loop for col orientation
-    static const int v = [] {
-        const char *e = std::getenv("AQR_COL_SCHEDULE");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-int direct_mode() {  // AQR_DIRECT=0: copy Z into Q first (A/B experiments)
-    static const int v = [] {
-        const char *e = std::getenv("AQR_DIRECT");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
-
-int defer_mode() {  // AQR_DEFER=0: separate r-row reduction launch (A/B experiments)
-    static const int v = [] {
-        const char *e = std::getenv("AQR_DEFER");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
 }
 
 
@@ -703,10 +671,7 @@ struct HostOut {
 
 // AQR_CATCHUP=0: one trailing launch (+ totals) per caught-up step; 2: the
 // cooperative launch with two grid barriers per step (A/B; read per call)
-int catchup_mode() {
-    const char *e = std::getenv("AQR_CATCHUP");
-    return e ? std::atoi(e) : 1;
-}
+int catchup_mode() { return knob("AQR_CATCHUP", 1); }  // read per call
 
 template <int RPT, bool HP, bool CGS>
 aqr_status launch_catchup_t(const aqr::CatchArgs &c, cudaStream_t s) {
@@ -818,10 +783,14 @@ struct Run {
 
     // Where step j's vector goes: HA x_j (xout), HP / naive p_j (pout_slot).
     double *xout(int64_t j) const { return (pp && !hp && !naive) ? pp->vall + j * m : xvec; }
+    // HP (row form): p_j is kept for the lazy x of later steps -- in vall
+    // (Pipe) or in X's column j, which col_lazy_norm_kernel read at step j
+    // and nothing reads afterwards.
     double *pout_slot(int64_t j) const {
         if (pp) return pp->vall + j * m;
-        return hp ? pring + (j & 1) * m : pvec;
+        return hp ? X + j * m : pvec;
     }
+    const double *pbase() const { return pp ? pp->vall : X; }
 
     // Bring the next chunk of Z in at step i (Pipe): wait for its H2D, form
     // its X = A Z (HP) / saved copy (CGS), then run steps 0 .. i-1's trailing
@@ -853,7 +822,7 @@ struct Run {
             c.Z0 = Z0;
             c.ldz0 = m;
             c.vall = pp->vall;
-            c.p_direct = (hp || naive) ? 1 : 0;
+            c.p_direct = (hp || naive) ? 1 : 0;  // HP: X is not caught up (lazy x)
             c.Rt = Rt;
             c.partial = pp->partial2;
             c.status = status;
@@ -861,18 +830,17 @@ struct Run {
             // one barrier per step when the totals fit in shared memory
             // (partial2 holds two parity buffers of the widest chunk)
             c.redundant = (catchup_mode() != 2 && w <= 4096) ? 1 : 0;
-            AQR_TRY(launch_catchup(c, hp, cgs, s));
+            AQR_TRY(launch_catchup(c, false, cgs, s));
             live = c1;
             return AQR_OK;
         }
         for (int64_t k = 0; k < i; ++k) {
             aqr::TrailArgs t = trail(k, c0, c1);
             t.qprev = k > 0 ? col(W, ldw, k - 1) : nullptr;
-            t.pprev = (hp && k > 0) ? pp->vall + (k - 1) * m : nullptr;
             t.psrc = pp->vall + k * m;
             t.rii = (hp || naive) ? nullptr : rt(k, k);
             t.partial = pp->partial2;
-            AQR_TRY(launch_trailing(t, hp, cgs, s));
+            AQR_TRY(launch_trailing(t, false, cgs, s));
         }
         live = c1;
         return AQR_OK;
@@ -883,7 +851,7 @@ struct Run {
     // breakdown / flag record (normalize(j), gram_schmidt.py:148-160).
     // Returns the columns holding the updated z and x.
     aqr_status norm_step(int64_t j, const double *pprev_col, const double *&zcol,
-                         const double *&xcol) {
+                         const double *&xcol, bool lazy = false) {
         double *z = col(W, ldw, j);
         const double *qprev = j > 0 ? col(W, ldw, j - 1) : nullptr;
         const double *r = j > 0 ? rt(j - 1, j) : nullptr;
@@ -891,7 +859,13 @@ struct Run {
         const aqr::RrowIn *pin = pending ? &rin : nullptr;
         pending = false;
         const double *zs = zread(j, j);  // column j as read at step j (nullptr: W)
-        if (hp) {
+        if (hp && lazy) {  // row form: x_j formed from X_j and p_0 .. p_{j-1}
+            double *xo = xvec + (j & 1) * m;
+            AQR_TRY(launch_col_lazy_norm(m, j, z, zs, qprev, col(X, m, j), pbase(), m, Rt + j, n, r, xo,
+                                         norm_out(j), pin, s));
+            zcol = (zs && !r) ? zs : z;
+            xcol = xo;
+        } else if (hp) {
             double *x = col(X, m, j);
             AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), true, s, pin, zs));
             zcol = (zs && !r) ? zs : z;  // without an update nothing was written to W
@@ -902,10 +876,7 @@ struct Run {
             double *xo = xout(j);
             const double *zx = zs ? zs : z;
             AQR_TRY(launch_csr(a->op, 1, zx, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
-            static const int rep = [] {  // diagnostics: idempotent repeats of the step
-                const char *e = std::getenv("AQR_SPMV_REPEAT");
-                return e ? std::atoi(e) : 0;
-            }();
+            const int rep = spmv_repeat();
             for (int k = 0; k < rep; ++k)
                 AQR_TRY(launch_csr(a->op, 1, zx, m, xo, m, qprev, r, zvec, norm_out(j), s, pin));
             ++mv;
@@ -954,12 +925,10 @@ struct Run {
         for (int64_t i = 0; i < n; ++i) {
             const auto hs = std::chrono::steady_clock::now();
             while (live <= i) AQR_TRY(make_live(i));
-            const double *pprev = (hp && i > 0) ? pout_slot(i - 1) : nullptr;
             const double *zcol = nullptr, *xcol = nullptr;
-            AQR_TRY(norm_step(i, pprev, zcol, xcol));
+            AQR_TRY(norm_step(i, nullptr, zcol, xcol, true));
             aqr::TrailArgs t = trail(i, i + 1, std::max<int64_t>(i + 1, live));
             t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
-            t.pprev = pprev;
             t.reverse = (int32_t)(i & 1);
             if (naive) {
                 // q_i first, then p_i = A q_i (lines 161-163)
@@ -975,10 +944,11 @@ struct Run {
                 t.pout = hp ? pout_slot(i) : nullptr;
             }
             {
-                static const bool dbg = std::getenv("AQR_DEBUG_TIMING") != nullptr;
+                const bool dbg = debug_timing() != 0;
                 const auto h0 = std::chrono::steady_clock::now();
                 const bool can_defer = (hp || csr_native) && i + 1 < n && defer_mode() != 0;
-                AQR_TRY(launch_trailing(t, hp, cgs, s, can_defer ? &pending : nullptr));
+                // HP too runs the Z-only pass: X is never rewritten (lazy x)
+                AQR_TRY(launch_trailing(t, false, cgs, s, can_defer ? &pending : nullptr));
                 pending_cols = t.jend - t.jbeg;
                 AQR_TRY(col_final(i));
                 if (dbg) {
@@ -1186,6 +1156,7 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
         r.pvec = r.P;
         r.pring = r.P;  // n >= 2: 2m <= mn; n = 1 uses slot 0 only
     }
+    if (r.hp) r.xvec = r.pring;  // HP row form: the lazy x_j ring (p_j lives in X / vall)
     cudaStream_t s = r.s;
 
     const bool direct = a->Z != a->Q && row_sched && !r.pp && direct_mode() != 0;
@@ -1208,7 +1179,7 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
         AQR_TRY(op_apply(a->op, n, direct ? a->Z : a->Q, direct ? a->ldz : a->ldq, r.X, m, s));
         r.mv += n;
     }
-    static const bool debug_timing = std::getenv("AQR_DEBUG_TIMING") != nullptr;
+    const bool dbg_timing = debug_timing() != 0;
     const auto t_loop = std::chrono::steady_clock::now();
     AQR_TRY(row_sched ? r.row_form() : r.col_form());
     aqr::finalize_r_kernel<<<(unsigned)((n * n + 255) / 256), 256, 0, s>>>(n, r.Rt, a->R, a->ldr);
@@ -1217,7 +1188,7 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
     AQR_CUDA(cudaMemcpyAsync(st.data(), r.status, 16 + 4 * n, cudaMemcpyDeviceToHost, s));
     const auto t_enq = std::chrono::steady_clock::now();
     AQR_CUDA(cudaStreamSynchronize(s));
-    if (debug_timing) {
+    if (dbg_timing) {
         const auto t_end = std::chrono::steady_clock::now();
         std::fprintf(stderr, "aqr_gs_factor: enqueue loop %.1f us, wait %.1f us\n",
                      std::chrono::duration<double, std::micro>(t_enq - t_loop).count(),
@@ -1258,10 +1229,7 @@ uint64_t aqr_pipe_workspace_bytes(int32_t family, int32_t variant, int32_t orien
 // ramping up from n/32 at the start): small final chunks still need a
 // catch-up over all previous steps each, small first ones start the D2H of
 // Q earlier, and neither beat uniform chunks.
-int pipe_sched_mode() {  // read per call
-    const char *e = std::getenv("AQR_PIPE_SCHED");
-    return e ? std::atoi(e) : 0;
-}
+int pipe_sched_mode() { return knob("AQR_PIPE_SCHED", 0); }  // read per call
 
 std::vector<int64_t> pipe_bounds(int64_t n, int64_t chunk_cols) {
     std::vector<int64_t> b{0};

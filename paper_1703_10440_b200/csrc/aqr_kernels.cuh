@@ -376,6 +376,13 @@ struct ColArgs {
     NormOut out;          // out.npart == nullptr: update only
     RrowIn rin;           // deferred r-row totals (rin.partial == nullptr: none)
     int32_t trace;        // AQR_TRACE builds: launch slot (-1 off)
+    // col_lazy_norm_kernel (HP, row form): x_j = X_j - sum_k r_{k,j} p_k
+    const double *P;      // p_0 .. p_{j-1}, ld ldp
+    int64_t ldp;
+    const double *rcol;   // r_{k,j} = rcol[k * rstride], k < j - 1 (final totals)
+    int64_t rstride;
+    int32_t nprev;        // j
+    double *xout;         // x_j goes here (X_j itself is only read)
 };
 
 // Column update (+ norm chains when out.npart): launched with exactly
@@ -437,6 +444,109 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
         norm_cta_partial(a.out, t, zz, xx, blockIdx.x);
         norm_last_cta(a.out, gridDim.x);
     }
+    rrow_rest(a.rin, blockIdx.x, gridDim.x);
+    trace_mark(a.trace, 2);
+}
+
+// HP, row form, with X read-only after the block apply.  project(k, j)
+// (gram_schmidt.py:139-145) updates X[:, j] at every step k < j, but
+// normalize(j) (:148-149) is the only reader of X[:, j]: here x_j is formed
+// when it is needed, X_j - r_{0,j} p_0 - r_{1,j} p_1 - ... - r_{j-1,j} p_{j-1},
+// in ascending k with the separately rounded multiply and subtract of the
+// reference's sub_scaled -- the very sequence of roundings the eager updates
+// would have applied, so the bits are unchanged.  Per step this reads the j
+// finished p columns (8 m j bytes) instead of reading and writing the n-1-j
+// trailing X columns at every step (16 m (n-1-j)): over the factorization
+// the X traffic halves and the whole HP step traffic drops by a quarter.
+// Also: the deferred update of z_j (r_{j-1,j} q_{j-1}), the norm partials
+// (z.x, z.z, x.x) on the canonical HP norm grid (same per-thread chains as
+// col_update_norm_kernel) and x_j -> a.xout for the trailing pass.
+constexpr int kLazyBlk = 4;    // owned 256-row blocks per load batch
+constexpr int kLazyK = 4;      // p columns per batch of loads
+constexpr int kLazyRs = 1024;  // r_{k,j} staged in shared memory per chunk
+__global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
+    trace_mark(a.trace, 0);
+    pdl_wait();
+    trace_mark(a.trace, 1);
+    if (failed(a.out.status)) return;
+    __shared__ double rs[kLazyRs];
+    const int32_t nk = a.nprev;
+    const bool upd = nk > 0;
+    const int64_t nblk = (a.m + kBlock - 1) / kBlock;
+    const int64_t G = gridDim.x;
+    // r_{j-1,j}: this kernel forms it from the trailing partials (RrowIn; CTA
+    // 0 stores it to R) or it is already final in R
+    const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
+    auto stage = [&](int kc, int kn) {
+        for (int k = threadIdx.x; k < kn; k += kBlock)
+            rs[k] = kc + k == nk - 1 ? rj : __ldcg(a.rcol + (int64_t)(kc + k) * a.rstride);
+    };
+    const bool one_chunk = nk <= kLazyRs;
+    if (one_chunk) stage(0, nk);
+    __syncthreads();
+    double t = 0.0, zz = 0.0, xx = 0.0;
+    for (int64_t b0 = blockIdx.x; b0 < nblk; b0 += G * kLazyBlk) {
+        int64_t row[kLazyBlk];
+        bool ok[kLazyBlk];
+        double z[kLazyBlk], x[kLazyBlk], q[kLazyBlk];
+#pragma unroll
+        for (int g = 0; g < kLazyBlk; ++g) {
+            row[g] = (b0 + g * G) * kBlock + threadIdx.x;
+            ok[g] = b0 + g * G < nblk && row[g] < a.m;
+            z[g] = ok[g] ? (a.zsrc ? a.zsrc[row[g]] : a.z[row[g]]) : 0.0;
+            q[g] = (ok[g] && upd) ? a.qprev[row[g]] : 0.0;
+            x[g] = ok[g] ? a.x[row[g]] : 0.0;
+        }
+        for (int kc = 0; kc < nk; kc += kLazyRs) {
+            const int kn = min(kLazyRs, nk - kc);
+            if (!one_chunk) {
+                __syncthreads();
+                stage(kc, kn);
+                __syncthreads();
+            }
+            const double *pc = a.P + (int64_t)kc * a.ldp;
+            int k = 0;
+#pragma unroll 2
+            for (; k + kLazyK <= kn; k += kLazyK) {
+                double pv[kLazyK][kLazyBlk];
+#pragma unroll
+                for (int u = 0; u < kLazyK; ++u)
+#pragma unroll
+                    for (int g = 0; g < kLazyBlk; ++g)
+                        pv[u][g] = ok[g] ? __ldcs(pc + (int64_t)(k + u) * a.ldp + row[g]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < kLazyK; ++u) {
+                    const double r = rs[k + u];
+#pragma unroll
+                    for (int g = 0; g < kLazyBlk; ++g) x[g] = __dsub_rn(x[g], __dmul_rn(r, pv[u][g]));
+                }
+            }
+            for (; k < kn; ++k) {
+                double pv[kLazyBlk];
+#pragma unroll
+                for (int g = 0; g < kLazyBlk; ++g) pv[g] = ok[g] ? __ldcs(pc + (int64_t)k * a.ldp + row[g]) : 0.0;
+                const double r = rs[k];
+#pragma unroll
+                for (int g = 0; g < kLazyBlk; ++g) x[g] = __dsub_rn(x[g], __dmul_rn(r, pv[g]));
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kLazyBlk; ++g) {
+            if (upd) {
+                z[g] = __dsub_rn(z[g], __dmul_rn(rj, q[g]));
+                if (ok[g]) a.z[row[g]] = z[g];
+            }
+            if (ok[g]) {
+                a.xout[row[g]] = x[g];
+                t = fma(z[g], x[g], t);
+                zz = fma(z[g], z[g], zz);
+                xx = fma(x[g], x[g], xx);
+            }
+        }
+    }
+    pdl_trigger();
+    norm_cta_partial(a.out, t, zz, xx, blockIdx.x);
+    norm_last_cta(a.out, gridDim.x);
     rrow_rest(a.rin, blockIdx.x, gridDim.x);
     trace_mark(a.trace, 2);
 }
@@ -852,26 +962,8 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused trailing pass, TMA-bulk pipelined (m >= 2048*148: RPT = 8, tiles of
-// 2048 rows = 16 KB per column).  Persistent: 2 CTAs per SM.  The step's
-// U = ntiles * t (tile, column) units are split into equal contiguous ranges,
-// one per CTA (unit u -> tile u / t, column jbeg + u % t), so every CTA moves
-// the same number of bytes and re-loads the step vectors only when its range
-// enters a new tile.  One producer warp streams the CTA's (tile, column)
-// blocks into a ring of shared-memory stages with cp.async.bulk + mbarrier
-// transaction counts (L2 evict-first: the stream must not evict the operator
-// and the step vectors); 8 consumer warps apply the deferred update, write
-// the column back (streaming stores) and accumulate p_i . z_j with the
-// canonical tile-partial structure (thread k owns rows k + 256 u).  The r row
-// totals are formed at the end by the last ceil(t / 32) CTAs to finish, which
-// wait for the whole grid (all CTAs are co-resident) -- one fence per CTA.
+// TMA bulk-copy helpers (cp.async.bulk + mbarrier transaction counts)
 // ---------------------------------------------------------------------------
-constexpr int kTmaRpt = 8;
-constexpr int kTmaTileRows = kBlock * kTmaRpt;  // 2048
-constexpr int kTmaTileBytes = kTmaTileRows * 8;  // 16 KB
-constexpr int kTmaThreads = kBlock + 32;         // + producer warp
-constexpr int kTmaMaxCols = 256;                 // rprev / run partials staged in smem
-
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -921,224 +1013,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
             " [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
             "l"(src), "r"(bytes), "r"(smem_u32(bar))
             : "memory");
-}
-__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-struct ConsumerBar {
-    __device__ void operator()() const { consumer_bar(); }
-};
-
-template <bool HP, bool CGS>
-struct TmaCfg {
-    static constexpr int kArrays = 1 + (HP ? 1 : 0) + (CGS ? 1 : 0);
-    static constexpr int kStageBytes = kArrays * kTmaTileBytes;
-    static constexpr int kStages = kArrays == 1 ? 5 : (kArrays == 2 ? 3 : 2);
-    static constexpr size_t kSmem = (size_t)kStages * kStageBytes + 2 * kStages * 8 +
-                                    (size_t)kTmaMaxCols * 8 /* rprev */ +
-                                    (size_t)kWarps * kTmaMaxCols * 8 /* run partials */ + 64;
-};
-
-// The CTA's unit range walked as runs of columns inside one tile, forwards
-// or backwards; the producer and the consumers walk the same sequence.
-struct RunWalker {
-    int64_t u0, u1, u;
-    int tcols;
-    bool rev;
-    __device__ RunWalker(int64_t units, int tcols_, bool rev_) : tcols(tcols_), rev(rev_) {
-        u0 = units * blockIdx.x / gridDim.x;
-        u1 = units * (blockIdx.x + 1) / gridDim.x;
-        u = rev ? u1 : u0;
-    }
-    // next run: tile, columns [c0, c1) (relative to jbeg); false when done
-    __device__ bool next(int64_t &tile, int &c0, int &c1) {
-        if (!rev) {
-            if (u >= u1) return false;
-            tile = u / tcols;
-            c0 = (int)(u % tcols);
-            { const int64_t e = c0 + (u1 - u); c1 = e < tcols ? (int)e : tcols; }
-            u += c1 - c0;
-        } else {
-            if (u <= u0) return false;
-            tile = (u - 1) / tcols;
-            c1 = (int)((u - 1) % tcols) + 1;
-            { const int64_t b = c1 - (u - u0); c0 = b > 0 ? (int)b : 0; }
-            u -= c1 - c0;
-        }
-        return true;
-    }
-};
-
-template <bool HP, bool CGS, bool HINT>
-__global__ void __launch_bounds__(kTmaThreads, 2) trailing_tma_kernel(TrailArgs a) {
-    using C = TmaCfg<HP, CGS>;
-
-    extern __shared__ __align__(128) unsigned char smem[];
-    double *stage_buf = reinterpret_cast<double *>(smem);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)C::kStages * C::kStageBytes);
-    uint64_t *empty = full + C::kStages;
-    double *rsm = reinterpret_cast<double *>(empty + C::kStages);  // [kTmaMaxCols]
-    double *wsum = rsm + kTmaMaxCols;                               // [kWarps][kTmaMaxCols]
-    __shared__ unsigned s_ticket;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = a.jend - a.jbeg;
-    const int tcols = t > 0 ? t : 1;  // t == 0: one vector-only unit per tile (q_i, p_i)
-    const int64_t units = (int64_t)a.ntiles * tcols;
-    const bool upd = a.qprev != nullptr;
-    const int64_t full_tiles = a.m / kTmaTileRows;  // tiles streamed by TMA
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < C::kStages; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, kWarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    pdl_wait();  // everything below reads the predecessors' results
-    if (failed(a.status)) return;
-    for (int c = threadIdx.x; c < t; c += kTmaThreads) rsm[c] = upd ? a.rprev[a.jbeg + c] : 0.0;
-    __syncthreads();
-
-    if (warp == kWarps) {  // ---------------- producer warp ----------------
-        if (lane == 0 && t > 0) {
-            const uint64_t pol = policy_evict_first();
-            uint32_t it = 0;
-            RunWalker wk(units, tcols, a.reverse != 0);
-            int64_t tile;
-            int c0, c1;
-            while (wk.next(tile, c0, c1)) {
-                if (tile >= full_tiles) continue;
-                const int64_t rbase = tile * kTmaTileRows;
-                for (int cc = 0; cc < c1 - c0; ++cc, ++it) {
-                    const int j = a.jbeg + (a.reverse ? c1 - 1 - cc : c0 + cc);
-                    const int s = it % C::kStages;
-                    const uint32_t ph = (it / C::kStages) & 1;
-                    mbar_wait(empty + s, ph ^ 1);
-                    mbar_expect_tx(full + s, C::kStageBytes);
-                    double *dst = stage_buf + (size_t)s * (C::kStageBytes / 8);
-                    bulk_g2s<HINT>(dst, a.W + (int64_t)j * a.ldw + rbase, kTmaTileBytes, full + s, pol);
-                    if (HP)
-                        bulk_g2s<HINT>(dst + kTmaTileRows, a.X + (int64_t)j * a.ldx + rbase,
-                                       kTmaTileBytes, full + s, pol);
-                    if (CGS)
-                        bulk_g2s<HINT>(dst + (C::kArrays - 1) * kTmaTileRows,
-                                       a.Z0 + (int64_t)j * a.ldz0 + rbase, kTmaTileBytes, full + s, pol);
-                }
-            }
-        }
-    } else {  // ---------------- consumer warps (256 threads) ----------------
-        uint32_t it = 0;
-        RunWalker wk(units, tcols, a.reverse != 0);
-        int64_t tile, cur_tile = -1;
-        int c0, c1;
-        double q[kTmaRpt], p[kTmaRpt], pp[kTmaRpt];
-        while (wk.next(tile, c0, c1)) {
-            const int64_t row0 = tile * kTmaTileRows + threadIdx.x;
-            if (tile != cur_tile) {  // the unit holding column jbeg stores q_i / p_i
-                const bool owner = (t == 0) || (a.reverse ? c0 == 0 : c0 == 0);
-                trail_vectors<kTmaRpt, HP>(a, row0, owner, q, p, pp);
-                cur_tile = tile;
-            } else if (c0 == 0) {
-                trail_vectors<kTmaRpt, HP>(a, row0, true, q, p, pp);
-            }
-            if (t == 0) continue;
-            const bool tma = tile < full_tiles;
-            const int ncols = c1 - c0;
-            // columns in batches of NB: one batched warp reduction per batch
-            constexpr int NB = (HP || CGS) ? 4 : 8;
-            for (int cc0 = 0; cc0 < ncols; cc0 += NB) {
-              double bacc[NB];
-#pragma unroll
-              for (int k = 0; k < NB; ++k) {
-                bacc[k] = 0.0;
-                const int cc = cc0 + k;
-                if (cc >= ncols) continue;
-                const int jr = a.reverse ? c1 - 1 - cc : c0 + cc;  // column relative to jbeg
-                const int j = a.jbeg + jr;
-                const double rj = rsm[jr];
-                double z[kTmaRpt], x[kTmaRpt], d[kTmaRpt];
-                if (tma) {
-                    const int s = it % C::kStages;
-                    const uint32_t ph = (it / C::kStages) & 1;
-                    mbar_wait(full + s, ph);
-                    const double *src = stage_buf + (size_t)s * (C::kStageBytes / 8);
-#pragma unroll
-                    for (int u = 0; u < kTmaRpt; ++u) {
-                        z[u] = src[threadIdx.x + u * kBlock];
-                        if (HP) x[u] = src[kTmaTileRows + threadIdx.x + u * kBlock];
-                        if (CGS) d[u] = src[(C::kArrays - 1) * kTmaTileRows + threadIdx.x + u * kBlock];
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty + s);
-                    ++it;
-                } else {
-#pragma unroll
-                    for (int u = 0; u < kTmaRpt; ++u) {
-                        const int64_t r = row0 + (int64_t)u * kBlock;
-                        const bool ok = r < a.m;
-                        z[u] = ok ? a.W[(int64_t)j * a.ldw + r] : 0.0;
-                        if (HP) x[u] = ok ? a.X[(int64_t)j * a.ldx + r] : 0.0;
-                        if (CGS) d[u] = ok ? a.Z0[(int64_t)j * a.ldz0 + r] : 0.0;
-                    }
-                }
-                double acc = 0.0;
-#pragma unroll
-                for (int u = 0; u < kTmaRpt; ++u) {
-                    const int64_t r = row0 + (int64_t)u * kBlock;
-                    const bool ok = r < a.m;
-                    if (upd) {
-                        z[u] = __dsub_rn(z[u], __dmul_rn(rj, q[u]));
-                        if (ok) __stcs(a.W + (int64_t)j * a.ldw + r, z[u]);
-                        if (HP) {
-                            x[u] = __dsub_rn(x[u], __dmul_rn(rj, pp[u]));
-                            if (ok) __stcs(a.X + (int64_t)j * a.ldx + r, x[u]);
-                        }
-                    }
-                    acc = fma(p[u], CGS ? d[u] : z[u], acc);
-                }
-                bacc[k] = acc;
-              }
-              // batched warp reduction of the NB columns (same tree as warp_sum)
-              const double tot = warp_sum_batch<NB>(bacc);
-              const int cc = cc0 + lane / (32 / NB);
-              if (lane % (32 / NB) == 0 && cc < ncols)
-                  wsum[warp * kTmaMaxCols + (a.reverse ? c1 - 1 - cc : c0 + cc)] = tot;
-            }
-            consumer_bar();
-            for (int c = c0 + threadIdx.x; c < c1; c += kBlock) {
-                double s = wsum[c];
-#pragma unroll
-                for (int ww = 1; ww < kWarps; ++ww) s = __dadd_rn(s, wsum[ww * kTmaMaxCols + c]);
-                a.partial[(int64_t)c * a.ntiles + tile] = s;
-            }
-            consumer_bar();
-        }
-        pdl_trigger();
-        // ---- r row totals: the last min(t, grid) CTAs to finish reduce ----
-        if (a.counters != nullptr && t > 0) {
-            const unsigned G = gridDim.x;
-            const unsigned K = min((unsigned)t, G);
-            __threadfence();
-            consumer_bar();
-            if (threadIdx.x == 0) s_ticket = atomicAdd(a.counters, 1u);
-            consumer_bar();
-            const unsigned ticket = s_ticket;
-            if (ticket >= G - K) {
-                if (threadIdx.x == 0)
-                    while (*(volatile unsigned *)a.counters < G) __nanosleep(64);
-                consumer_bar();
-                __threadfence();
-                const int r = (int)(ticket - (G - K));
-                for (int c = r; c < t; c += (int)K)
-                    block_totals<1>(a.partial + (int64_t)c * a.ntiles, a.ntiles, a.ntiles, a.rout + c,
-                                    wsum, ConsumerBar());
-                __threadfence();
-                consumer_bar();
-                if (threadIdx.x == 0 && atomicAdd(a.counters + 1, 1u) == K - 1) {
-                    a.counters[0] = 0u;  // every CTA has passed its ticket: reset for the next launch
-                    a.counters[1] = 0u;
-                }
-            }
-        }
-    }
 }
 // ---------------------------------------------------------------------------
 // Reference kernel namespace (backend.kernels()): dot, sub_scaled, div_scalar
@@ -1769,132 +1643,10 @@ __global__ void __launch_bounds__(kGvRows + 32, 2)
     if (threadIdx.x < rows) y[r0 + threadIdx.x] = acc;
 }
 
-// Y = A X (k columns), shared-memory tiled, every output accumulated over
-// ascending j with separate rounding: bitwise equal to k matvecs
-// (apply_block_dense, _kernels_impl.py:35-47).
-constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
-__global__ void __launch_bounds__(256)
-    dense_gemm_kernel(int64_t m, int64_t ncols, int64_t k, const double *__restrict__ A, int64_t lda,
-                      const double *__restrict__ X, int64_t ldx, double *__restrict__ Y,
-                      int64_t ldy) {
-    __shared__ double As[kGemmBK][kGemmBM + 1];
-    __shared__ double Xs[kGemmBK][kGemmBN + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4x4 each
-    const int64_t i0 = (int64_t)blockIdx.x * kGemmBM, c0 = (int64_t)blockIdx.y * kGemmBN;
-    double acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    for (int64_t j0 = 0; j0 < ncols; j0 += kGemmBK) {
-        for (int e = threadIdx.x; e < kGemmBM * kGemmBK; e += 256) {
-            const int ii = e % kGemmBM, jj = e / kGemmBM;
-            const int64_t gi = i0 + ii, gj = j0 + jj;
-            As[jj][ii] = (gi < m && gj < ncols) ? A[gi + gj * lda] : 0.0;
-        }
-        for (int e = threadIdx.x; e < kGemmBN * kGemmBK; e += 256) {
-            const int jj = e % kGemmBK, cc = e / kGemmBK;
-            const int64_t gj = j0 + jj, gc = c0 + cc;
-            Xs[jj][cc] = (gj < ncols && gc < k) ? X[gj + gc * ldx] : 0.0;
-        }
-        __syncthreads();
-        const int kmax = (ncols - j0) < kGemmBK ? (int)(ncols - j0) : kGemmBK;
-        for (int jj = 0; jj < kmax; ++jj) {
-            double av[4], xv[4];
-#pragma unroll
-            for (int a = 0; a < 4; ++a) av[a] = As[jj][ty + 16 * a];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) xv[b] = Xs[jj][tx + 16 * b];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(av[a], xv[b]));
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int64_t gi = i0 + ty + 16 * a, gc = c0 + tx + 16 * b;
-            if (gi < m && gc < k) Y[gi + gc * ldy] = acc[a][b];
-        }
-}
-
-// Larger register tiles for the FP64 pipe: CTA 128 x 64 outputs, 256 threads,
-// 8 x 4 outputs per thread (12 shared loads per 64 FP64 instructions instead
-// of 8 per 32), the next 16-deep slice of A and X prefetched into registers
-// while the current one is consumed (double-buffered shared memory).  Same
-// per-output order (ascending j, separately rounded multiply and add).
+// Y = A X (k columns): 128 x 64 output tiles, 16-deep k slices, every
+// output accumulated over ascending j with separate rounding -- bitwise equal
+// to k matvecs (apply_block_dense, _kernels_impl.py:35-47).
 constexpr int kG2BM = 128, kG2BN = 64, kG2BK = 16;
-__global__ void __launch_bounds__(256, 1)
-    dense_gemm2_kernel(int64_t m, int64_t ncols, int64_t k, const double *__restrict__ A, int64_t lda,
-                       const double *__restrict__ X, int64_t ldx, double *__restrict__ Y, int64_t ldy) {
-    __shared__ double As[2][kG2BK][kG2BM];
-    __shared__ double Xs[2][kG2BK][kG2BN];  // 48 KB total with As (static limit)
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int64_t i0 = (int64_t)blockIdx.x * kG2BM, c0 = (int64_t)blockIdx.y * kG2BN;
-    double acc[8][4];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    // per-thread load slots: A: 8 elements (rows tid & 127, slices (tid >> 7) + 2u),
-    // X: 4 elements (slice tid & 15, columns (tid >> 4) + 16u)
-    double ra[8], rx[4];
-    auto load = [&](int64_t j0) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int ii = tid & 127, jj = (tid >> 7) + 2 * u;
-            const int64_t gi = i0 + ii, gj = j0 + jj;
-            ra[u] = (gi < m && gj < ncols) ? __ldg(A + gi + gj * lda) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int jj = tid & 15, cc = (tid >> 4) + 16 * u;
-            const int64_t gj = j0 + jj, gc = c0 + cc;
-            rx[u] = (gj < ncols && gc < k) ? __ldg(X + gj + gc * ldx) : 0.0;
-        }
-    };
-    auto store = [&](int buf) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) As[buf][(tid >> 7) + 2 * u][tid & 127] = ra[u];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) Xs[buf][tid & 15][(tid >> 4) + 16 * u] = rx[u];
-    };
-    load(0);
-    store(0);
-    __syncthreads();
-    int buf = 0;
-    for (int64_t j0 = 0; j0 < ncols; j0 += kG2BK) {
-        const bool more = j0 + kG2BK < ncols;
-        if (more) load(j0 + kG2BK);
-        const int kmax = (ncols - j0) < kG2BK ? (int)(ncols - j0) : kG2BK;
-        for (int jj = 0; jj < kmax; ++jj) {
-            double av[8], xv[4];
-#pragma unroll
-            for (int a = 0; a < 8; ++a) av[a] = As[buf][jj][ty + 16 * a];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) xv[b] = Xs[buf][jj][tx + 16 * b];
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] = __dadd_rn(acc[a][b], __dmul_rn(av[a], xv[b]));
-        }
-        if (more) {
-            store(buf ^ 1);
-            __syncthreads();
-            buf ^= 1;
-        }
-    }
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int64_t gi = i0 + ty + 16 * a, gc = c0 + tx + 16 * b;
-            if (gi < m && gc < k) Y[gi + gc * ldy] = acc[a][b];
-        }
-}
 
 // Same tiles, operands streamed into a 3-stage shared-memory ring with
 // cp.async (no register staging: <= 128 registers, 2 CTAs per SM).

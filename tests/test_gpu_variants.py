@@ -1,13 +1,16 @@
 """Every kernel variant kept behind an experiment knob computes the same bits.
 
-The knobs are read once per process (include/aqr_b200.h, DESIGN.md section
-8), so each variant runs in a subprocess and its factors are compared
-bitwise with the default build's: the TMA-bulk trailing kernel (with and
-without the L2 hint), the unpipelined SpMV step, the separate R-row
-reduction launch, launches without programmatic dependent launch, the
-materialized copy of Z, the column-oriented loop for the col methods
-(by default they run the row-oriented step schedule), and the per-step
-catch-up launches of the host-input pipeline.
+The knobs exist only in the experiments build (libaqr_b200_exp.so,
+-DAQR_EXPERIMENTS; the shipped libaqr_b200.so compiles them to their
+defaults) and are read once per process, so each variant runs in a
+subprocess on the experiments build and its factors are compared bitwise
+with the shipped library's: other trailing-pass column widths, the
+unpipelined SpMV step, the separate R-row reduction launch, launches
+without programmatic dependent launch, the materialized copy of Z, the
+column-oriented loop for the col methods (by default they run the
+row-oriented step schedule -- for HP that is also the eagerly updated X
+against the shipped lazy x), and the per-step catch-up launches of the
+host-input pipeline.
 """
 
 import os
@@ -48,9 +51,15 @@ np.savez({path!r}, **out)
 """
 
 
-def _run(env_extra, path):
+EXP_LIB = os.path.join(REPO, "paper_1703_10440_b200", "libaqr_b200_exp.so")
+
+
+def _run(env_extra, path, lib=None):
     env = dict(os.environ)
     env.update(env_extra)
+    env.pop("AQR_LIB_PATH", None)
+    if lib:
+        env["AQR_LIB_PATH"] = lib
     code = SCRIPT.format(repo=REPO, path=str(path))
     subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
     return np.load(path)
@@ -62,8 +71,7 @@ def default_factors(tmp_path_factory):
 
 
 @pytest.mark.parametrize("knobs", [
-    {"AQR_TRAIL_VARIANT": "1"},
-    {"AQR_TRAIL_VARIANT": "4"},
+    {},
     {"AQR_TRAIL_VARIANT": "3"},
     {"AQR_TRAIL_VARIANT": "5"},
     {"AQR_TRAIL_VARIANT": "6"},
@@ -80,6 +88,13 @@ def default_factors(tmp_path_factory):
     {"AQR_CATCHUP": "0"},
 ])
 def test_variant_bitwise_equal_default(default_factors, knobs, tmp_path):
-    got = _run(knobs, tmp_path / "variant.npz")
+    got = _run(knobs, tmp_path / "variant.npz", lib=EXP_LIB)
     for key in default_factors.files:
         assert np.array_equal(got[key], default_factors[key]), (knobs, key)
+
+
+def test_shipped_library_ignores_knobs(default_factors, tmp_path):
+    """A stray experiment variable does not change the shipped library's schedule."""
+    got = _run({"AQR_COL_SCHEDULE": "1", "AQR_DEFER": "0", "AQR_TRAIL_VARIANT": "5"}, tmp_path / "s.npz")
+    for key in default_factors.files:
+        assert np.array_equal(got[key], default_factors[key]), key

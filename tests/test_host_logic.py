@@ -120,8 +120,11 @@ def _pipe_chunks(n, chunk, sched=None):
 
     env = dict(os.environ)
     env.pop("AQR_PIPE_SCHED", None)
-    if sched is not None:
+    env.pop("AQR_LIB_PATH", None)
+    if sched is not None:  # the alternative schedules exist in the experiments build only
         env["AQR_PIPE_SCHED"] = str(sched)
+        env["AQR_LIB_PATH"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                           "paper_1703_10440_b200", "libaqr_b200_exp.so")
     out = subprocess.run([sys.executable, "-c", code], env=env, check=True, capture_output=True, text=True,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     return [int(v) for v in out.stdout.split()]

@@ -1,8 +1,9 @@
 # e2e of the host-input pipeline for chunk widths / schedules, alternating
+export AQR_LIB_PATH=${AQR_LIB_PATH:-paper_1703_10440_b200/libaqr_b200_exp.so}  # knobs: experiments build only
 meth=${1:-mgs-ha-row}
 for rep in 1 2; do
   for cfg in "AQR_CHUNK_COLS=0" "AQR_CHUNK_COLS=4" "AQR_PIPE_SCHED=1" "AQR_CHUNK_COLS=2"; do
     printf "%-20s " "$cfg"
-    env $cfg python bench.py --method $meth --no-cpu-baseline --steps 10 --warmup 3 | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('value %.0f e2e %.0f ms_e2e %.2f' % (d['value'], d['e2e']['value'], 64e3/d['e2e']['value']))"
+    env $cfg python bench.py --config 2 --method $meth --no-cpu-baseline --steps 10 --warmup 3 | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('value %.0f e2e %.0f ms_e2e %.2f' % (d['value'], d['e2e']['value'], 64e3/d['e2e']['value']))"
   done
 done

@@ -1,4 +1,5 @@
 # trailing-pass column grouping (AQR_TRAIL_CTAS) A/B with per-launch times
+export AQR_LIB_PATH=${AQR_LIB_PATH:-paper_1703_10440_b200/libaqr_b200_exp.so}  # knobs: experiments build only
 meth=${1:-mgs-ha-row}
 for c in 4 2 3 6 8; do
   echo "== AQR_TRAIL_CTAS=$c"

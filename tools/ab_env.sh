@@ -1,4 +1,5 @@
 # A/B of environment knobs, alternating: bash tools/ab_env.sh METHOD "ENV=a" "ENV=b" ...
+export AQR_LIB_PATH=${AQR_LIB_PATH:-paper_1703_10440_b200/libaqr_b200_exp.so}  # knobs: experiments build only
 meth=$1; shift
 for rep in 1 2 3; do for cfg in "$@"; do
   printf "%-10s %-24s " "$meth" "$cfg"

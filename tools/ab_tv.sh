@@ -1,4 +1,5 @@
 # A/B of trailing-kernel variants (AQR_TRAIL_VARIANT), alternating
+export AQR_LIB_PATH=${AQR_LIB_PATH:-paper_1703_10440_b200/libaqr_b200_exp.so}  # knobs: experiments build only
 meth=$1; shift
 for rep in 1 2; do for tv in "$@"; do
   printf "%-10s tv=%s " "$meth" "$tv"
