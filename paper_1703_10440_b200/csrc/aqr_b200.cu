@@ -763,7 +763,22 @@ struct Run {
     }
     double *rt(int64_t i, int64_t j) const { return Rt + i * n + j; }
 
+    // A user operator (callback) sees exactly the reference's calls: the
+    // reference raises BreakdownError inside normalize(f) (gram_schmidt.py:
+    // 153-154), so no apply follows the one that fed the failing column.  The
+    // breakdown record is on the device; before each callback the stream is
+    // drained and it is read (the callback costs a host round trip anyway).
+    // After a breakdown the callback is skipped; the device kernels already
+    // early-exit on the record.
+    bool stopped = false;
     aqr_status mv1(const double *x, double *y) {
+        if (a->op->kind == AQR_OP_CALLBACK && !stopped) {
+            int32_t st0 = -1;
+            AQR_CUDA(cudaMemcpyAsync(&st0, status, sizeof st0, cudaMemcpyDeviceToHost, s));
+            AQR_CUDA(cudaStreamSynchronize(s));
+            stopped = st0 >= 0;
+        }
+        if (stopped) return AQR_OK;
         AQR_TRY(op_apply(a->op, 1, x, m, y, m, s));
         ++mv;
         return AQR_OK;

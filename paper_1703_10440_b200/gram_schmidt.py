@@ -246,8 +246,8 @@ def _gs_factor(Z, op, family, variant, orientation):
     expected = _expected_mv(variant, n, fail_col)
     if native:
         op.mv_count += expected
-    elif op.mv_count - mv_before > expected:
-        op.mv_count = mv_before + expected
+    # a user operator counted its own calls: exactly the reference's, also
+    # after a breakdown (the library stops calling it at the failing column)
     if status == _lib.AQR_EBREAKDOWN:
         raise BreakdownError(fail_col, float(a.fail_val))
     if status == _lib.AQR_EDIM:
