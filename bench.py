@@ -111,17 +111,50 @@ def config_dict(cfg, method, m, n, nnz, world):
     return d
 
 
-def step_bytes(variant, m, n, bytes_A, lazy_x=True):
-    """Algorithmic HBM bytes of one factorization (one-pass look-ahead model).
+TRAIL_WIN = 6  # write-back period of the windowed trailing passes (AQR_TRAIL_WIN default)
+X_WIN = 8      # HP X catch-up period (AQR_X_WIN default)
 
-    HP with ``lazy_x`` (the single-GPU row form): X = A Z is never rewritten;
-    step j forms x_j from X_j and the j finished p columns (col_lazy_norm_kernel),
-    so the X term is sum_j 8 m j = T / 2 instead of SURVEY 8d's second T
-    (``lazy_x=False``: the eager model, which the peer-memory path still runs)."""
+
+def survey_bytes(variant, m, n, bytes_A):
+    """SURVEY.md 8d's one-pass look-ahead model: every trailing element (and
+    for HP every trailing X element) read and written once per step."""
     T = 8 * m * n * (n - 1)
     mv = bytes_A + 16 * m
     return {"ha": T + n * mv + 32 * m * n, "naive": T + 2 * n * mv + 32 * m * n,
-            "hp": (T + T // 2 if lazy_x else 2 * T) + (bytes_A + 16 * m * n) + 32 * m * n}[variant]
+            "hp": 2 * T + (bytes_A + 16 * m * n) + 32 * m * n}[variant]
+
+
+def step_bytes(variant, m, n, bytes_A, win=TRAIL_WIN, xwin=X_WIN):
+    """Algorithmic HBM bytes of one single-GPU row-form factorization as this
+    build schedules it (the host loop of csrc/aqr_b200.cu, Run::row_form):
+
+    * trailing pass i (t = n-1-i columns): every stored element read once,
+      written only on write-back passes (every ``win``-th; else only column
+      i+1), the q window (i - zbase columns), p_i, and q_i / p_i stored;
+    * HA / naive: the operator products (A once + z in + x out) and the
+      column update / norm vectors as in SURVEY 8d;
+    * HP: X = A Z once (A + Z in + X out); step j forms x_j from the stored
+      X_j and the p columns it lags behind; every ``xwin`` steps the stored
+      X columns catch up (read + write + the p window)."""
+    T, zbase, xbase = 0, 0, 0
+    for i in range(n):
+        t = n - 1 - i
+        w = i - zbase if t > 0 else 0
+        store = w >= win
+        T += 8 * m * (t + (t if store else (min(t, 1) if w > 0 else 0)) + w + 1)
+        T += 8 * m * (3 if variant == "hp" else 2)  # zsrc read, q_i (+ p_i) stored
+        if store:
+            zbase = i
+    if variant == "hp":
+        X = bytes_A + 16 * m * n  # X = A Z
+        for j in range(n):
+            X += 8 * m * ((j - xbase) + 1 + 1 + (2 if j else 0) + 1)  # p window, X_j, z_j (+q, z store), x_j
+            if j - xbase >= xwin and j + 1 < n:
+                X += 8 * m * (2 * (n - 1 - j) + (j - xbase))
+                xbase = j
+        return T + X
+    mv = bytes_A + 16 * m
+    return T + (2 if variant == "naive" else 1) * n * mv + 16 * m * n
 
 
 def measured_peaks():
@@ -420,7 +453,7 @@ def run_b200(args, rank, world, local_rank):
         "frac": achieved / peak if achieved else None, "traffic": traffic,
         "traffic_unit": "GB per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
         "traffic_source": traffic_src,
-        "kernel": "trailing_kernel", "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+        "kernel": "trailing_w_kernel", "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
         "timed": "inside the timed region" if timer_inside else "separate pass of K steps",
         "launches_per_step": nl.value / args.steps if nl.value else 0,
         "kernel_ms_per_step": kms.value / args.steps, "kernel_share_of_step": share,
@@ -429,10 +462,10 @@ def run_b200(args, rank, world, local_rank):
     sb = step_bytes(variant, m, n, bytes_A)
     step_gbs = sb / (ms_per_step / 1e3) / 1e9
     roofline["step"] = {"achieved": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": sb}
-    if variant == "hp":  # what the eager schedule would have to move in the same time
-        eager = step_bytes(variant, m, n, bytes_A, lazy_x=False)
-        roofline["step"]["survey_8d_bytes"] = eager
-        roofline["step"]["survey_8d_equivalent_gbs"] = eager / (ms_per_step / 1e3) / 1e9
+    # what SURVEY 8d's eager one-pass schedule would have to move in the same time
+    eager = survey_bytes(variant, m, n, bytes_A)
+    roofline["step"]["survey_8d_bytes"] = eager
+    roofline["step"]["survey_8d_equivalent_gbs"] = eager / (ms_per_step / 1e3) / 1e9
 
     # ---- end to end: numpy Z in, numpy Q / R out, through the public API ----
     e2e = None
@@ -589,7 +622,7 @@ def run_b200_distributed(args, rank, world, local_rank):
     gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
     dist.all_gather(gathered, per_rank)
     bytes_A = 12 * 449_455_096 + 4 * (m + 1)
-    sb = step_bytes("hp", m, n, bytes_A, lazy_x=False)
+    sb = survey_bytes("hp", m, n, bytes_A)  # the peer-memory path runs the eager schedule
     step_gbs = sb / (ms_per_step / 1e3) / 1e9
     e2e = None
     if not args.no_e2e:

@@ -101,7 +101,7 @@ aqr_status ensure_smem(K kernel, size_t bytes) {
 
 // ---- kernel timer (bench.py's roofline leg) ---------------------------------
 // Slot 0: fused trailing pass; slot 1: fused SpMV step; slot 2: column
-// update + norm.  When enabled, a CUDA event pair is recorded around every
+// update + norm; slot 3: HP X catch-up; slot 4: block apply (k > 1).  When enabled, a CUDA event pair is recorded around every
 // launch of those kernels on the launching stream.
 struct KernelTimer {
     struct Rec {
@@ -170,9 +170,8 @@ AQR_KNOB(carveout_pct, "AQR_CARVEOUT", -1)
 AQR_KNOB(pdl_mode, "AQR_PDL", 1)
 // AQR_LDG_REVERSE=0: the trailing kernel always walks forwards.
 AQR_KNOB(ldg_reverse_mode, "AQR_LDG_REVERSE", 1)
-// AQR_TRAIL_VARIANT: columns per iteration of the trailing kernel (0 = the
-// default: 2 for MGS / CGS-HP, 1 for MGS-HP; 3 = 4 columns, 5 = 1 column,
-// 6 = HP with 2 columns).
+// AQR_TRAIL_VARIANT=6: the X-carrying (HP column loop) trailing pass with two
+// columns per iteration for MGS (default one).
 #ifdef AQR_EXPERIMENTS
 AQR_KNOB(trail_variant, "AQR_TRAIL_VARIANT", 0)
 #endif
@@ -190,6 +189,14 @@ AQR_KNOB(direct_mode, "AQR_DIRECT", 1)
 AQR_KNOB(defer_mode, "AQR_DEFER", 1)
 // AQR_SPMV_REPEAT=k: k idempotent repeats of every fused SpMV step (diagnostics).
 AQR_KNOB(spmv_repeat, "AQR_SPMV_REPEAT", 0)
+// AQR_TRAIL_WIN=b: the row form's trailing block is written back every b-th
+// pass (trailing_w_kernel; 1 = every pass, the eager schedule).
+AQR_KNOB(trail_win_knob, "AQR_TRAIL_WIN", 6)
+int trail_win() { return std::min(std::max(trail_win_knob(), 1), 8); }
+// AQR_X_WIN=b: HP row form, the stored X columns catch up every b steps
+// (0 = never: x_j formed from all j finished p columns).
+AQR_KNOB(x_win_knob, "AQR_X_WIN", 8)
+int64_t x_win() { return x_win_knob() > 0 ? x_win_knob() : (int64_t)1 << 40; }
 // AQR_DEBUG_TIMING=1: host-side enqueue timings on stderr.
 AQR_KNOB(debug_timing, "AQR_DEBUG_TIMING", 0)
 
@@ -364,8 +371,23 @@ aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx
     return launched("dense_gemm3_kernel");
 }
 
+aqr_status op_apply_impl(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                         int64_t ldy, cudaStream_t s);
+
+// Block applies (k > 1) are timed in slot 4: A once + X in + Y out.
 aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                     int64_t ldy, cudaStream_t s) {
+    if (!op || k <= 1 || op->kind == AQR_OP_CALLBACK) return op_apply_impl(op, k, X, ldx, Y, ldy, s);
+    const double abytes = op->kind == AQR_OP_DENSE ? 8.0 * (double)op->m * (double)(op->ncols > 0 ? op->ncols : op->m)
+                                                   : 12.0 * (double)op->nnz + 4.0 * (double)(op->m + 1);
+    const long tix = timer_begin(4, abytes + 16.0 * (double)op->m * (double)k, s);
+    const aqr_status st = op_apply_impl(op, k, X, ldx, Y, ldy, s);
+    timer_end(tix, s);
+    return st;
+}
+
+aqr_status op_apply_impl(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                         int64_t ldy, cudaStream_t s) {
     if (!op) return set_err(AQR_EARG, "null operator");
     switch (op->kind) {
         case AQR_OP_DENSE:
@@ -426,7 +448,7 @@ aqr_status launch_col_update_norm(int64_t m, double *z, const double *qprev, dou
 
 // HP row form, step j: x_j = X_j - sum_{k<j} r_{k,j} p_k, the deferred z_j
 // update and the norm partials (col_lazy_norm_kernel).
-aqr_status launch_col_lazy_norm(int64_t m, int64_t j, double *z, const double *zsrc, const double *qprev,
+aqr_status launch_col_lazy_norm(int64_t m, int64_t j, int64_t nprev, double *z, const double *zsrc, const double *qprev,
                                 const double *Xj, const double *P, int64_t ldp, const double *rcol,
                                 int64_t rstride, const double *r, double *xout, const aqr::NormOut &out,
                                 const aqr::RrowIn *rin, cudaStream_t s) {
@@ -446,23 +468,59 @@ aqr_status launch_col_lazy_norm(int64_t m, int64_t j, double *z, const double *z
     a.ldp = ldp;
     a.rcol = rcol;
     a.rstride = rstride;
-    a.nprev = (int32_t)j;
+    a.nprev = (int32_t)nprev;
     a.xout = xout;
     const int64_t nt = aqr::norm_tiles(m, true);
     if (nt == 0) return AQR_OK;
     ensure_carveout(aqr::col_lazy_norm_kernel);
-    // bytes: p_0..p_{j-1}, X_j, z_j (+ q_{j-1} and the z_j store), x_j store
-    const long tix = timer_begin(2, (double)m * (8.0 * (double)j + 8.0 + 8.0 + (j > 0 ? 16.0 : 0.0) + 8.0), s);
+    // bytes: p_{j-nprev}..p_{j-1}, X_j, z_j (+ q_{j-1} and the z_j store), x_j store
+    const long tix = timer_begin(2, (double)m * (8.0 * (double)nprev + 8.0 + 8.0 + (j > 0 ? 16.0 : 0.0) + 8.0), s);
     launch_pdl(aqr::col_lazy_norm_kernel, (unsigned)nt, aqr::kBlock, 0, s, a);
     timer_end(tix, s);
     return launched("col_lazy_norm_kernel");
 }
 
+// X_j -= sum_k r_kj p_k over k = kbeg .. kbeg+nk-1 for j in [jbeg, jend)
+// (x_catchup_kernel); P = p_kbeg (columns at stride ldp), R = row kbeg of Rt.
+aqr_status launch_x_catchup(int64_t m, double *X, int64_t ldx, int64_t jbeg, int64_t jend, const double *P,
+                            int64_t ldp, const double *R, int64_t rstride, int64_t nk, const int32_t *status,
+                            cudaStream_t s) {
+    if (jend <= jbeg || nk <= 0 || m <= 0) return AQR_OK;
+    aqr::XCatchArgs a;
+    a.m = m;
+    a.X = X;
+    a.ldx = ldx;
+    a.jbeg = (int32_t)jbeg;
+    a.jend = (int32_t)jend;
+    a.P = P;
+    a.ldp = ldp;
+    a.R = R;
+    a.rstride = rstride;
+    a.nk = (int32_t)nk;
+    a.status = status;
+    const int64_t groups = (jend - jbeg + aqr::kXcCols - 1) / aqr::kXcCols;
+    const int64_t rows = (m + aqr::kBlock - 1) / aqr::kBlock;
+    const long tix = timer_begin(3, (double)m * (16.0 * (double)(jend - jbeg) + 8.0 * (double)nk), s);
+    launch_pdl(aqr::x_catchup_kernel, dim3((unsigned)(groups * rows)), aqr::kBlock, 0, s, a);
+    timer_end(tix, s);
+    return launched("x_catchup_kernel");
+}
+
 // Algorithmic HBM bytes of one trailing launch: every trailing element read
 // once (and written once when the deferred update applies), the step's
 // vectors once.  Re-reads caused by column grouping are not counted.
-double trailing_bytes(const aqr::TrailArgs &a, bool hp, bool cgs) {
+// Windowed passes (trailing_w_kernel): every trailing element read once
+// (CGS: its Z0 element, and z only where written), written only when the
+// pass stores it (store_all, or column jbeg); the q window and the step's
+// vectors once per row.
+double trailing_bytes(const aqr::TrailArgs &a, bool hp, bool cgs, bool windowed) {
     const double m = (double)a.m, t = (double)std::max(0, a.jend - a.jbeg);
+    if (windowed) {
+        const double stored = a.win <= 0 ? 0.0 : (a.store_all ? t : std::min(t, 1.0));
+        const double cols = cgs ? 8.0 * t + 16.0 * stored : 8.0 * t + 8.0 * stored;
+        const double vec = 8.0 /* psrc */ + 8.0 * a.win + (a.qout ? 16.0 : 0.0) + (a.pout ? 8.0 : 0.0);
+        return m * (cols + vec);
+    }
     const bool upd = a.qprev != nullptr;
     double per_col = 8.0 + (upd ? 8.0 : 0.0) + ((hp && upd) ? 16.0 : 0.0) + (cgs ? 8.0 : 0.0);
     double vec = 8.0 /* psrc */ + (upd ? 8.0 : 0.0) + ((hp && upd) ? 8.0 : 0.0) +
@@ -510,37 +568,53 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
     if (ldg_reverse_mode() == 0) a.reverse = 0;
 
-    const long tix = timer_begin(0, trailing_bytes(a, hp, cgs), s);
+    if (!hp) {  // the Z-only pass runs windowed (trailing_w_kernel); one eager projection = window 1
+        if (a.win == 0 && a.qprev != nullptr) {
+            a.win = 1;
+            a.qwin = a.qprev;
+            a.rwin = a.rprev;
+            a.rstride = 0;
+            a.store_all = 1;
+        }
+        a.qprev = nullptr;  // (trail_prefetch: the window's first column instead)
+        if (a.win > 0) a.qprev = a.qwin + (int64_t)(a.win - 1) * a.ldw;
+    }
+    const long tix = timer_begin(0, trailing_bytes(a, hp, cgs, !hp), s);
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
+    if (!hp) {
+        const int rpt = big ? 8 : 1;
+        const size_t smw = aqr::trail_w_smem(rpt, std::max(a.cpg, 1), a.win);
+#define LAUNCHW(RPT, CU, CGS)                                                            \
+    do {                                                                                 \
+        AQR_TRY(ensure_smem(aqr::trailing_w_kernel<RPT, CU, CGS>, smw));                 \
+        launch_pdl(aqr::trailing_w_kernel<RPT, CU, CGS>, grid, aqr::kBlock, smw, s, a); \
+    } while (0)
+        if (big) { if (cgs) LAUNCHW(8, 2, true); else LAUNCHW(8, 2, false); }
+        else     { if (cgs) LAUNCHW(1, 4, true); else LAUNCHW(1, 4, false); }
+#undef LAUNCHW
+        goto done;
+    }
+    {
     const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
 #define LAUNCH(RPT, CU, HP, CGS)                                                           \
     do {                                                                                   \
         AQR_TRY(ensure_smem(aqr::trailing_kernel<RPT, CU, HP, CGS>, smem));                \
         launch_pdl(aqr::trailing_kernel<RPT, CU, HP, CGS>, grid, aqr::kBlock, smem, s, a); \
     } while (0)
+    // Passes that carry X (the HP column loop): MGS one column per iteration
+    // (128 registers, 2 CTAs/SM: 2.8 % faster than two at 164 registers /
+    // 1 CTA/SM on config 2), CGS two (144 registers either way; 12 % faster).
     if (big) {
 #ifdef AQR_EXPERIMENTS
-        // AQR_TRAIL_VARIANT: 3 = four columns per iteration, 5 = one, 6 = HP with two
-        const int tv = trail_variant();
-        if (tv == 6 && hp && !cgs) { LAUNCH(8, 2, true, false); goto done; }
-        if (tv == 5 && !hp) { if (cgs) LAUNCH(8, 1, false, true); else LAUNCH(8, 1, false, false); goto done; }
-        if (tv == 3 && !hp) { if (cgs) LAUNCH(8, 4, false, true); else LAUNCH(8, 4, false, false); goto done; }
+        if (trail_variant() == 6 && !cgs) { LAUNCH(8, 2, true, false); goto done; }  // MGS-HP, two columns
 #endif
-        // Z-only passes (HA, naive and the lazy-x HP row form): two columns per
-        // iteration (120 registers, 2 CTAs/SM).  Passes that also carry X (the
-        // HP column loop): MGS one column per iteration (128 registers, 2
-        // CTAs/SM: 2.8 % faster than two at 164 registers / 1 CTA/SM on
-        // config 2), CGS two (144 registers either way; 12 % faster).
-        if (hp) { if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 1, true, false); }
-        else    { if (cgs) LAUNCH(8, 2, false, true); else LAUNCH(8, 2, false, false); }
+        if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 1, true, false);
     } else {
-        if (hp) { if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false); }
-        else    { if (cgs) LAUNCH(1, 4, false, true); else LAUNCH(1, 4, false, false); }
+        if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false);
     }
 #undef LAUNCH
-#ifdef AQR_EXPERIMENTS
+    }
 done:
-#endif
     timer_end(tix, s);
     AQR_TRY(launched("trailing_kernel"));
     if (a.counters != nullptr && ncols > 0) {  // totals pending
@@ -673,29 +747,24 @@ struct HostOut {
 // cooperative launch with two grid barriers per step (A/B; read per call)
 int catchup_mode() { return knob("AQR_CATCHUP", 1); }  // read per call
 
-template <int RPT, bool HP, bool CGS>
+template <int RPT, bool CGS>
 aqr_status launch_catchup_t(const aqr::CatchArgs &c, cudaStream_t s) {
-    // wsum [kWarps][2] + the redundant totals rs[w] (rounded up to 8: block_totals<8>)
-    constexpr int kCu = HP ? 1 : 2;  // columns per unit (catchup_kernel)
-    const size_t smem = sizeof(double) * (2 * aqr::kWarps + (c.redundant ? ((c.w + 7) / 8) * 8 : 0));
-    AQR_TRY(ensure_smem(aqr::catchup_kernel<RPT, HP, CGS>, smem));
+    constexpr int kCu = 2;  // columns per unit (catchup_kernel)
+    const size_t smem = aqr::catch_smem(RPT, c.w, c.win, c.redundant != 0);
+    AQR_TRY(ensure_smem(aqr::catchup_kernel<RPT, CGS>, smem));
     int o = 0;
-    AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, aqr::catchup_kernel<RPT, HP, CGS>, aqr::kBlock, smem));
+    AQR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, aqr::catchup_kernel<RPT, CGS>, aqr::kBlock, smem));
     const int64_t units = (int64_t)c.ntiles * ((c.w + kCu - 1) / kCu);
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)sm_count() * std::max(1, o)));
     aqr::CatchArgs cc = c;
     void *args[] = {&cc};
-    AQR_CUDA(cudaLaunchCooperativeKernel((const void *)aqr::catchup_kernel<RPT, HP, CGS>, grid, aqr::kBlock, args, smem, s));
+    AQR_CUDA(cudaLaunchCooperativeKernel((const void *)aqr::catchup_kernel<RPT, CGS>, grid, aqr::kBlock, args, smem, s));
     return launched("catchup_kernel");
 }
 
-aqr_status launch_catchup(const aqr::CatchArgs &c, bool hp, bool cgs, cudaStream_t s) {
-    if (aqr::rows_per_thread(c.m) == 8) {
-        if (hp) return cgs ? launch_catchup_t<8, true, true>(c, s) : launch_catchup_t<8, true, false>(c, s);
-        return cgs ? launch_catchup_t<8, false, true>(c, s) : launch_catchup_t<8, false, false>(c, s);
-    }
-    if (hp) return cgs ? launch_catchup_t<1, true, true>(c, s) : launch_catchup_t<1, true, false>(c, s);
-    return cgs ? launch_catchup_t<1, false, true>(c, s) : launch_catchup_t<1, false, false>(c, s);
+aqr_status launch_catchup(const aqr::CatchArgs &c, bool cgs, cudaStream_t s) {
+    if (aqr::rows_per_thread(c.m) == 8) return cgs ? launch_catchup_t<8, true>(c, s) : launch_catchup_t<8, false>(c, s);
+    return cgs ? launch_catchup_t<1, true>(c, s) : launch_catchup_t<1, false>(c, s);
 }
 
 // Host-input pipeline (aqr_gs_factor_pinned): Z arrives in column chunks on
@@ -718,6 +787,14 @@ struct Run {
     HostOut *ho = nullptr;
     Pipe *pp = nullptr;
     int64_t live = 0;  // columns [0, live) are resident and caught up
+    // Row form, windowed trailing passes: the stored trailing columns hold
+    // z_j^(zbase) (projections 0 .. zbase-1 applied); the pass of step i
+    // applies zbase .. i-1 in registers (trailing_w_kernel).
+    int64_t zbase = 0;
+    // HP row form: the stored X columns j >= live-from hold x_j^(xbase)
+    // (x_catchup_kernel brings them forward every few steps); step j forms
+    // x_j^(j) from them and p_xbase .. p_{j-1} (col_lazy_norm_kernel).
+    int64_t xbase = 0;
     // Direct mode (row form, Z distinct from Q): the input Z is read in place
     // by steps 0 and 1 -- the first writes of the trailing columns happen in
     // the trailing pass of step 1 -- so the copy Zw = Z (gram_schmidt.py:131)
@@ -832,8 +909,6 @@ struct Run {
             c.k1 = (int32_t)i;
             c.W = W;
             c.ldw = ldw;
-            c.X = X;
-            c.ldx = m;
             c.Z0 = Z0;
             c.ldz0 = m;
             c.vall = pp->vall;
@@ -845,9 +920,12 @@ struct Run {
             // one barrier per step when the totals fit in shared memory
             // (partial2 holds two parity buffers of the widest chunk)
             c.redundant = (catchup_mode() != 2 && w <= 4096) ? 1 : 0;
-            AQR_TRY(launch_catchup(c, false, cgs, s));
+            // windowed (the r rows of the window in shared memory) for chunks of <= 512 columns
+            c.win = w <= 512 ? trail_win() : 1;
+            AQR_TRY(launch_catchup(c, cgs, s));
             live = c1;
-            return AQR_OK;
+            zbase = i - 1;  // the chunk holds z^(i-1): projection i-1 is left to step i
+            return x_chunk(i, c0, c1);
         }
         for (int64_t k = 0; k < i; ++k) {
             aqr::TrailArgs t = trail(k, c0, c1);
@@ -858,6 +936,17 @@ struct Run {
             AQR_TRY(launch_trailing(t, false, cgs, s));
         }
         live = c1;
+        zbase = i > 0 ? i - 1 : 0;
+        return x_chunk(i, c0, c1);
+    }
+
+    // HP: a chunk's X = A Z arrives at x^(0); with R rows 0 .. i-1 of its
+    // columns final (catch-up) it is brought to x^(i) in one pass.
+    aqr_status x_chunk(int64_t i, int64_t c0, int64_t c1) {
+        xbase = 0;
+        if (!hp || i == 0) return AQR_OK;
+        AQR_TRY(launch_x_catchup(m, X, m, c0, c1, pbase(), m, rt(0, 0), n, i, status, s));
+        xbase = i;
         return AQR_OK;
     }
 
@@ -876,8 +965,15 @@ struct Run {
         const double *zs = zread(j, j);  // column j as read at step j (nullptr: W)
         if (hp && lazy) {  // row form: x_j formed from X_j and p_0 .. p_{j-1}
             double *xo = xvec + (j & 1) * m;
-            AQR_TRY(launch_col_lazy_norm(m, j, z, zs, qprev, col(X, m, j), pbase(), m, Rt + j, n, r, xo,
-                                         norm_out(j), pin, s));
+            AQR_TRY(launch_col_lazy_norm(m, j, j - xbase, z, zs, qprev, col(X, m, j), pbase() + xbase * m, m,
+                                         rt(xbase, j), n, r, xo, norm_out(j), pin, s));
+            // every x_win() steps: the stored columns j+1 .. live-1 catch up
+            // to x^(j) (R rows < j are final once this step's kernel ran)
+            if (j - xbase >= x_win() && j + 1 < live) {
+                AQR_TRY(launch_x_catchup(m, X, m, j + 1, live, pbase() + xbase * m, m, rt(xbase, 0), n, j - xbase,
+                                         status, s));
+                xbase = j;
+            }
             zcol = (zs && !r) ? zs : z;
             xcol = xo;
         } else if (hp) {
@@ -943,7 +1039,14 @@ struct Run {
             const double *zcol = nullptr, *xcol = nullptr;
             AQR_TRY(norm_step(i, nullptr, zcol, xcol, true));
             aqr::TrailArgs t = trail(i, i + 1, std::max<int64_t>(i + 1, live));
-            t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
+            // deferred projections zbase .. i-1; the block is written back
+            // when the window is full (the last pass has no trailing columns)
+            t.win = t.jend > t.jbeg ? (int32_t)(i - zbase) : 0;
+            t.store_all = t.win >= trail_win() ? 1 : 0;
+            t.qwin = t.win > 0 ? col(W, ldw, zbase) : nullptr;
+            t.rwin = t.win > 0 ? rt(zbase, 0) : nullptr;
+            t.rstride = n;
+            t.Wsrc = (Zin && zbase == 0) ? Zin : nullptr;  // nothing written back yet: read Z in place
             t.reverse = (int32_t)(i & 1);
             if (naive) {
                 // q_i first, then p_i = A q_i (lines 161-163)
@@ -965,6 +1068,7 @@ struct Run {
                 // HP too runs the Z-only pass: X is never rewritten (lazy x)
                 AQR_TRY(launch_trailing(t, false, cgs, s, can_defer ? &pending : nullptr));
                 pending_cols = t.jend - t.jbeg;
+                if (t.store_all) zbase = i;
                 AQR_TRY(col_final(i));
                 if (dbg) {
                     const auto h1 = std::chrono::steady_clock::now();
@@ -1011,7 +1115,7 @@ aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, 
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
     const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
-    const long tix = timer_begin(0, trailing_bytes(a, HP, CGS), s);
+    const long tix = timer_begin(0, trailing_bytes(a, HP, CGS, false), s);
     if (aqr::rows_per_thread(a.m) == 8) {
         constexpr int CU = (HP && !CGS) ? 1 : 2;  // as launch_trailing: MGS-HP one column per iteration
         AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, CU, HP, CGS>, smem));

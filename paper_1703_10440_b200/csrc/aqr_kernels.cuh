@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
     trace_mark(a.trace, 1);
     if (failed(a.out.status)) return;
     __shared__ double rs[kLazyRs];
-    const int32_t nk = a.nprev;
-    const bool upd = nk > 0;
+    const int32_t nk = a.nprev;  // lazy terms k = j - nk .. j-1 (X_j holds x_j^(j - nk))
+    const bool upd = a.r != nullptr || a.rin.partial != nullptr;  // z_j's deferred r_{j-1,j} q_{j-1}
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x;
     // r_{j-1,j}: this kernel forms it from the trailing partials (RrowIn; CTA
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
     const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
     auto stage = [&](int kc, int kn) {
         for (int k = threadIdx.x; k < kn; k += kBlock)
-            rs[k] = kc + k == nk - 1 ? rj : __ldcg(a.rcol + (int64_t)(kc + k) * a.rstride);
+            rs[k] = (kc + k == nk - 1 && upd) ? rj : __ldcg(a.rcol + (int64_t)(kc + k) * a.rstride);
     };
     const bool one_chunk = nk <= kLazyRs;
     if (one_chunk) stage(0, nk);
@@ -549,6 +549,72 @@ __global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
     norm_last_cta(a.out, gridDim.x);
     rrow_rest(a.rin, blockIdx.x, gridDim.x);
     trace_mark(a.trace, 2);
+}
+
+// HP row form: catch-up of the stored X columns.  With x formed lazily
+// (col_lazy_norm_kernel) step j reads p_k for every k the stored X_j lags
+// behind; every few steps (and when a chunk of the host-input pipeline
+// arrives) the stored columns j in [jbeg, jend) are brought forward by the
+// projections k = kbeg .. kbeg + nk - 1: x -= r_kj p_k in ascending k with
+// the reference's separately rounded multiply and subtract (gram_schmidt.py:
+// 143-145) -- the same rounding sequence, so the bits of every x_j are
+// unchanged; only where the terms are applied moves.  One thread per row
+// keeps CU columns in registers and streams the p_k of its row; the column
+// groups are the grid's fastest dimension, so the CTAs sharing a row block
+// run together and the p_k rows come from L2 after the first.
+struct XCatchArgs {
+    int64_t m;
+    double *X;
+    int64_t ldx;
+    int32_t jbeg, jend;
+    const double *P;  // p_kbeg, p_kbeg+1, ... at stride ldp
+    int64_t ldp;
+    const double *R;  // r_{kbeg + k, j} = R[k * rstride + j]
+    int64_t rstride;
+    int32_t nk;
+    const int32_t *status;
+};
+constexpr int kXcCols = 8;  // columns per thread
+constexpr int kXcK = 32;    // r_kj staged per chunk of k
+constexpr int kXcPf = 8;    // p_k loads in flight per thread
+__global__ void __launch_bounds__(kBlock, 4) x_catchup_kernel(XCatchArgs a) {
+    __shared__ double rs[kXcK][kXcCols];
+    pdl_wait();
+    if (failed(a.status)) return;
+    const int groups = (a.jend - a.jbeg + kXcCols - 1) / kXcCols;  // column groups fastest
+    const int64_t r = (int64_t)(blockIdx.x / groups) * kBlock + threadIdx.x;
+    const bool ok = r < a.m;
+    const int j0 = a.jbeg + (int)(blockIdx.x % groups) * kXcCols;
+    const int nc = min(kXcCols, a.jend - j0);
+    double x[kXcCols];
+#pragma unroll
+    for (int c = 0; c < kXcCols; ++c) x[c] = (ok && c < nc) ? a.X[(int64_t)(j0 + c) * a.ldx + r] : 0.0;
+    for (int kc = 0; kc < a.nk; kc += kXcK) {
+        const int kn = min(kXcK, a.nk - kc);
+        __syncthreads();
+        for (int e = threadIdx.x; e < kXcK * kXcCols; e += kBlock) {
+            const int k = e / kXcCols, c = e - k * kXcCols;
+            rs[k][c] = (k < kn && c < nc) ? __ldg(a.R + (int64_t)(kc + k) * a.rstride + j0 + c) : 0.0;
+        }
+        __syncthreads();
+        for (int k0 = 0; k0 < kn; k0 += kXcPf) {
+            double pv[kXcPf];
+#pragma unroll
+            for (int u = 0; u < kXcPf; ++u)
+                pv[u] = (ok && k0 + u < kn) ? a.P[(int64_t)(kc + k0 + u) * a.ldp + r] : 0.0;
+#pragma unroll
+            for (int u = 0; u < kXcPf; ++u) {
+                if (k0 + u < kn) {
+#pragma unroll
+                    for (int c = 0; c < kXcCols; ++c) x[c] = __dsub_rn(x[c], __dmul_rn(rs[k0 + u][c], pv[u]));
+                }
+            }
+        }
+    }
+    pdl_trigger();
+#pragma unroll
+    for (int c = 0; c < kXcCols; ++c)
+        if (ok && c < nc) a.X[(int64_t)(j0 + c) * a.ldx + r] = x[c];
 }
 
 // Standalone totals of the norm partials (step API / multi-GPU driver).
@@ -646,6 +712,13 @@ struct TrailArgs {
     double *rout;         // totals: rout[j - jbeg] (row i of Rt from column jbeg)
     const int32_t *status;
     int32_t trace;        // AQR_TRACE builds: launch slot (-1 off)
+    // windowed pass (trailing_w_kernel): projections i-win .. i-1 are applied
+    // to the stored columns (state z^(i-win)) before the dots
+    int32_t win;
+    int32_t store_all;    // write every column back at z^(i) (else only column jbeg)
+    const double *qwin;   // q_{i-win}; q_k at qwin + (k - i + win) * ldw
+    const double *rwin;   // r_{i-win, j} = rwin[j]; row k at + (k - i + win) * rstride
+    int64_t rstride;
 };
 
 // Load the step vectors of one tile into registers; group 0 stores q_i/p_i.
@@ -801,21 +874,179 @@ __global__ void __launch_bounds__(kBlock, HP ? AQR_HP_MINB : 1) trailing_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// Windowed trailing pass (row form, Z only): deferred projections
+// ---------------------------------------------------------------------------
+// project(k, j) (gram_schmidt.py:139-145) rewrites every trailing column at
+// every step, but step i only needs z_j^(i) -- z_j after the projections
+// 0 .. i-1 -- inside its dot products r_ij = p_i . z_j^(i).  The stored
+// trailing columns are kept at an older state z_j^(s) (s <= i, the "base"),
+// and the pass of step i re-forms z_j^(i) in registers by applying the
+// win = i - s deferred projections z -= r_kj q_k, k = s .. i-1, in ascending
+// k with the reference's separately rounded multiply and subtract: the very
+// sequence of roundings the eager updates apply, so every z_j^(i) -- and the
+// factors -- are bitwise unchanged.  Only every b-th pass writes the
+// trailing block back (store_all; the base becomes i); the other passes read
+// it once and write only column jbeg = i+1, the next one to be normalized.
+// Per step the trailing traffic drops from a read and a write of every
+// element to a read plus 1/b of a write; the price is win extra multiply-
+// subtract pairs per element (FP64 pipe, well below its rate at b <= 8) and
+// the q_k window staged per tile.
+//
+// Shared memory (dynamic): wsum [kWarps][cpg], rsm [win][cpg] (r_kj of the
+// CTA's columns), qs [win][RPT][kBlock] (thread-private rows of q_k).
+__host__ __device__ inline size_t trail_w_smem(int rpt, int cpg, int win) {
+    return sizeof(double) * ((size_t)kWarps * cpg + (size_t)win * cpg + (size_t)win * rpt * kBlock);
+}
+
+template <int RPT, int CU, bool CGS>
+__device__ __forceinline__ void trail_body_w(const TrailArgs &a, int tile, int group, double *smem) {
+    const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
+    const int cbeg = a.jbeg + group * a.cpg;
+    const int cend = min(a.jend, cbeg + a.cpg);
+    const int nc = cend - cbeg;
+    const int win = a.win;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *wsum = smem;
+    double *rsm = wsum + kWarps * a.cpg;
+    double *qs = rsm + win * a.cpg;
+
+    bool ok[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) ok[u] = row0 + (int64_t)u * kBlock < a.m;
+    // step vectors: p_i (group 0 stores q_i, p_i), the q window (thread-private
+    // rows) and the CTA's r_kj
+    double p[RPT];
+    {
+        double ps[RPT], zs[RPT];
+        const bool sq = group == 0 && a.qout != nullptr, sp = group == 0 && a.pout != nullptr;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int64_t r = row0 + (int64_t)u * kBlock;
+            ps[u] = ok[u] ? a.psrc[r] : 0.0;
+            zs[u] = (ok[u] && sq) ? a.zsrc[r] : 0.0;
+        }
+        for (int k = 0; k < win; ++k) {
+            double qv[RPT];
+#pragma unroll
+            for (int u = 0; u < RPT; ++u)
+                qv[u] = ok[u] ? __ldcg(a.qwin + (int64_t)k * a.ldw + row0 + (int64_t)u * kBlock) : 0.0;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) qs[(k * RPT + u) * kBlock + threadIdx.x] = qv[u];
+        }
+        for (int e = threadIdx.x; e < win * nc; e += kBlock) {
+            const int k = e / nc, c = e - k * nc;
+            rsm[k * a.cpg + c] = __ldcg(a.rwin + (int64_t)k * a.rstride + cbeg + c);
+        }
+        const double rii = a.rii ? *a.rii : 1.0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int64_t r = row0 + (int64_t)u * kBlock;
+            p[u] = a.rii ? ps[u] / rii : ps[u];
+            if (ok[u] && sq) a.qout[r] = zs[u] / rii;
+            if (ok[u] && sp) a.pout[r] = p[u];
+        }
+    }
+    __syncthreads();
+    const double *zb = a.Wsrc ? a.Wsrc : a.W;
+    const int64_t ldzb = a.Wsrc ? a.ldwsrc : a.ldw;
+
+    for (int j0 = cbeg; j0 < cend; j0 += CU) {
+        // CGS reads z only where it is written (the dots use Z0)
+        const bool needz = !CGS || (win > 0 && (a.store_all || j0 == a.jbeg));
+        double z[CU][RPT], d0[CGS ? CU : 1][RPT];
+#pragma unroll
+        for (int c = 0; c < CU; ++c) {
+            const int j = j0 + c;
+            const bool cj = j < cend;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) {
+                const int64_t r = row0 + (int64_t)u * kBlock;
+                z[c][u] = (needz && cj && ok[u]) ? zb[(int64_t)j * ldzb + r] : 0.0;
+                if (CGS) d0[c][u] = (cj && ok[u]) ? a.Z0[(int64_t)j * a.ldz0 + r] : 0.0;
+            }
+        }
+        if (needz) {
+#pragma unroll 1
+            for (int k = 0; k < win; ++k) {
+                double qv[RPT], rk[CU];
+#pragma unroll
+                for (int u = 0; u < RPT; ++u) qv[u] = qs[(k * RPT + u) * kBlock + threadIdx.x];
+#pragma unroll
+                for (int c = 0; c < CU; ++c) rk[c] = j0 + c < cend ? rsm[k * a.cpg + (j0 + c - cbeg)] : 0.0;
+#pragma unroll
+                for (int c = 0; c < CU; ++c)
+#pragma unroll
+                    for (int u = 0; u < RPT; ++u) z[c][u] = __dsub_rn(z[c][u], __dmul_rn(rk[c], qv[u]));
+            }
+            if (win > 0) {
+#pragma unroll
+                for (int c = 0; c < CU; ++c) {
+                    const int j = j0 + c;
+                    if (j < cend && (a.store_all || j == a.jbeg))
+#pragma unroll
+                        for (int u = 0; u < RPT; ++u)
+                            if (ok[u]) a.W[(int64_t)j * a.ldw + row0 + (int64_t)u * kBlock] = z[c][u];
+                }
+            }
+        }
+        double acc[CU];
+#pragma unroll
+        for (int c = 0; c < CU; ++c) {
+            acc[c] = 0.0;
+#pragma unroll
+            for (int u = 0; u < RPT; ++u) acc[c] = fma(p[u], CGS ? d0[CGS ? c : 0][u] : z[c][u], acc[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < CU; ++c) {
+            const double s = warp_sum(acc[c]);
+            if (lane == 0 && j0 + c < cend) wsum[warp * a.cpg + (j0 + c - cbeg)] = s;
+        }
+    }
+    pdl_trigger();
+    __syncthreads();
+    for (int c = threadIdx.x; c < nc; c += kBlock) {
+        double s = wsum[c];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) s = __dadd_rn(s, wsum[w * a.cpg + c]);
+        a.partial[(int64_t)(cbeg - a.jbeg + c) * a.ntiles + tile] = s;
+    }
+}
+
+template <int RPT, int CU, bool CGS>
+__global__ void __launch_bounds__(kBlock, 1) trailing_w_kernel(TrailArgs a) {
+    trace_mark(a.trace, 0);
+    trail_prefetch<RPT>(a, a.reverse ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x,
+                        a.reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y);
+    pdl_wait();
+    trace_mark(a.trace, 1);
+    if (failed(a.status)) return;
+    extern __shared__ double smem_w[];
+    const int tile = a.reverse ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+    const int group = a.reverse ? (int)(gridDim.y - 1 - blockIdx.y) : (int)blockIdx.y;
+    trail_body_w<RPT, CU, CGS>(a, tile, group, smem_w);
+    trace_mark(a.trace, 2);
+}
+
+// ---------------------------------------------------------------------------
 // Catch-up of a newly arrived chunk of columns (host-input pipeline): the
 // trailing passes of steps 0 .. k1-1 restricted to the chunk, in ONE
 // cooperative launch -- per step a pass over the (tile, column) units, a grid
 // barrier, the chunk's R-row totals (block_totals, CTA b: column b), a grid
-// barrier.  The chunk (w x m) stays in L2 across the steps; the launches and
-// drains of 2 k1 small kernels disappear.  Per unit the same chain and
-// trees as trail_body, totals as rrow_reduce_kernel: bitwise identical.
+// barrier.  The launches and drains of 2 k1 small kernels disappear.  Per
+// unit the same chain and trees as trail_body_w, totals as
+// rrow_reduce_kernel: bitwise identical.
+//
+// Windowed like trailing_w_kernel: the chunk's stored columns stay at
+// z^(sc) while step k applies the projections sc .. k-1 in registers (q
+// window per tile in shared memory, r rows of the window staged per step);
+// they are written back every win-th step and at the last one, so the
+// chunk leaves at z^(k1-1) -- what the step loop expects.
 // ---------------------------------------------------------------------------
 struct CatchArgs {
     int64_t m, n;
     int32_t ntiles, c0, w, k1;
     double *W;
     int64_t ldw;
-    double *X;  // HP
-    int64_t ldx;
     const double *Z0;  // CGS
     int64_t ldz0;
     const double *vall;  // per-step vectors, ld m: HA x_k (p_k = x_k / r_kk), HP / naive p_k
@@ -825,25 +1056,39 @@ struct CatchArgs {
     const int32_t *status;
     int32_t trace;      // AQR_TRACE builds: launch slot (-1 off)
     int32_t redundant;  // per-CTA totals, one grid barrier per step (smem: w doubles)
+    int32_t win;        // write-back period (1: every step)
 };
 
-// Tiles per column loaded together by the catch-up's per-CTA totals (build
-// knob: 2 keeps 2 CTAs/SM with a few spilled bytes; 1 no spills, two round trips).
+// Dynamic shared memory: wsum [kWarps][2], rs [wpad] (redundant totals),
+// rsm [win][wpad] (the window's r rows), qs [win][RPT][kBlock].
+__host__ __device__ inline int catch_wpad(int w) { return ((w + 7) / 8) * 8; }
+__host__ __device__ inline size_t catch_smem(int rpt, int w, int win, bool redundant) {
+    return sizeof(double) * ((size_t)2 * kWarps + (redundant ? catch_wpad(w) : 0) +
+                             (size_t)win * catch_wpad(w) + (size_t)win * rpt * kBlock);
+}
+
 #ifndef AQR_CATCHUP_REVERSE
 #define AQR_CATCHUP_REVERSE 1
 #endif
+// Tiles per column loaded together by the catch-up's per-CTA totals (build
+// knob: 2 keeps 2 CTAs/SM with a few spilled bytes; 1 no spills, two round trips).
 #ifndef AQR_CATCHUP_TOT_H
 #define AQR_CATCHUP_TOT_H 2
 #endif
-template <int RPT, bool HP, bool CGS>
+template <int RPT, bool CGS>
 __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     trace_mark(a.trace, 0);
     trace_mark(a.trace, 1);
     if (failed(a.status)) return;  // uniform: set before this launch
-    extern __shared__ double wsum[];  // [kWarps][2], then rs[w] (redundant totals)
+    constexpr int CU = 2;          // columns per unit
+    extern __shared__ double smc[];
+    const int wpad = catch_wpad(a.w);
+    double *wsum = smc;
     double *rs = wsum + 2 * kWarps;
+    double *rsm = rs + (a.redundant ? wpad : 0);
+    double *qs = rsm + a.win * wpad;
     __shared__ double tot1[1];
     __shared__ double sm1[kWarps];
     __shared__ double sm8[8 * kWarps];
@@ -853,31 +1098,38 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
     // between two buffers by step parity -- one grid barrier per step
     // instead of two around a totals phase on w CTAs.
     const int64_t pstride = (int64_t)a.w * a.ntiles;
+    int sc = 0;  // the chunk's stored columns hold z^(sc)
     for (int k = 0; k < a.k1; ++k) {
-        const bool upd = k > 0;
+        const int win = k - sc;  // projections sc .. k-1 applied in registers
+        const bool store = win > 0 && (win >= a.win || k + 1 == a.k1);
         double *part = a.partial + (a.redundant ? (int64_t)(k & 1) * pstride : 0);
-        if (a.redundant && upd) {
+        if (a.redundant && k > 0) {
             const double *prev = a.partial + (int64_t)((k - 1) & 1) * pstride;
             for (int cb = 0; cb < a.w; cb += 8) {
-                block_totals<8, SyncAll, AQR_CATCHUP_TOT_H>(prev + (int64_t)cb * a.ntiles, a.ntiles, a.ntiles, rs + cb, sm8,
-                                            SyncAll());
+                block_totals<8, SyncAll, AQR_CATCHUP_TOT_H>(prev + (int64_t)cb * a.ntiles, a.ntiles, a.ntiles, rs + cb,
+                                                            sm8, SyncAll());
             }
             if (blockIdx.x == 0)
                 for (int c = threadIdx.x; c < a.w; c += kBlock) a.Rt[(int64_t)(k - 1) * a.n + a.c0 + c] = rs[c];
         }
+        // r rows sc .. k-1 of the chunk (row k-1: this CTA's own totals when
+        // redundant; the others were stored and published by a grid barrier)
+        for (int e = threadIdx.x; e < win * a.w; e += kBlock) {
+            const int kk = e / a.w, c = e - kk * a.w;
+            rsm[kk * wpad + c] = (a.redundant && kk == win - 1) ? rs[c]
+                                                                : __ldcg(a.Rt + (int64_t)(sc + kk) * a.n + a.c0 + c);
+        }
+        __syncthreads();
         const double rii = a.p_direct ? 1.0 : __ldcg(a.Rt + (int64_t)k * a.n + k);
-        const double *qprev = upd ? a.W + (int64_t)(k - 1) * a.ldw : nullptr;
         const double *psrc = a.vall + (int64_t)k * a.m;
-        const double *pprev = (HP && upd) ? a.vall + (int64_t)(k - 1) * a.m : nullptr;
         // units (tile, CU columns), tile-major; CTA b walks the contiguous
         // range [U b / G, U (b + 1) / G) (balanced to one unit) and reloads
         // the step vectors only when the range enters a new tile
-        constexpr int CU = HP ? 1 : 2;  // HP carries x too: one column per unit (registers)
         const int ng = (a.w + CU - 1) / CU;
         const int64_t U = (int64_t)a.ntiles * ng;
         const int64_t ub = U * blockIdx.x / gridDim.x, ue = U * (blockIdx.x + 1) / gridDim.x;
         int cur = -1;
-        double q[RPT], p[RPT], pp[RPT];
+        double p[RPT];
         bool ok[RPT];
         // odd steps walk the range backwards: a step starts on the units the
         // previous one touched last (still in L2); per unit independent, so
@@ -887,20 +1139,27 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
             const int64_t u = back ? ub + ue - 1 - uu : uu;
             const int tile = (int)(u / ng), c0 = (int)(u % ng) * CU;
             const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
-            if (tile != cur) {
+            if (tile != cur) {  // thread-private rows: no barrier needed
                 cur = tile;
 #pragma unroll
                 for (int v = 0; v < RPT; ++v) {
                     const int64_t r = row0 + (int64_t)v * kBlock;
                     ok[v] = r < a.m;
-                    q[v] = (ok[v] && upd) ? __ldcg(qprev + r) : 0.0;
                     const double ps = ok[v] ? __ldcg(psrc + r) : 0.0;
                     p[v] = a.p_direct ? ps : ps / rii;
-                    pp[v] = (HP && ok[v] && upd) ? __ldcg(pprev + r) : 0.0;
+                }
+                for (int kk = 0; kk < win; ++kk) {
+                    double qv[RPT];
+#pragma unroll
+                    for (int v = 0; v < RPT; ++v)
+                        qv[v] = ok[v] ? __ldcg(a.W + (int64_t)(sc + kk) * a.ldw + row0 + (int64_t)v * kBlock) : 0.0;
+#pragma unroll
+                    for (int v = 0; v < RPT; ++v) qs[(kk * RPT + v) * kBlock + threadIdx.x] = qv[v];
                 }
             }
             {
-                double z[CU][RPT], x[CU][RPT], acc[CU];
+                const bool needz = !CGS || store;
+                double z[CU][RPT], d0[CGS ? CU : 1][RPT], acc[CU];
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {
                     const int j = a.c0 + c0 + c;
@@ -908,31 +1167,37 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
 #pragma unroll
                     for (int v = 0; v < RPT; ++v) {
                         const int64_t r = row0 + (int64_t)v * kBlock;
-                        z[c][v] = (cj && ok[v]) ? __ldcg(a.W + (int64_t)j * a.ldw + r) : 0.0;
-                        if (HP) x[c][v] = (cj && ok[v] && upd) ? __ldcg(a.X + (int64_t)j * a.ldx + r) : 0.0;
+                        z[c][v] = (needz && cj && ok[v]) ? __ldcg(a.W + (int64_t)j * a.ldw + r) : 0.0;
+                        if (CGS) d0[c][v] = (cj && ok[v]) ? __ldcg(a.Z0 + (int64_t)j * a.ldz0 + r) : 0.0;
+                    }
+                }
+                if (needz) {
+#pragma unroll 1
+                    for (int kk = 0; kk < win; ++kk) {
+                        double qv[RPT], rk[CU];
+#pragma unroll
+                        for (int v = 0; v < RPT; ++v) qv[v] = qs[(kk * RPT + v) * kBlock + threadIdx.x];
+#pragma unroll
+                        for (int c = 0; c < CU; ++c) rk[c] = c0 + c < a.w ? rsm[kk * wpad + c0 + c] : 0.0;
+#pragma unroll
+                        for (int c = 0; c < CU; ++c)
+#pragma unroll
+                            for (int v = 0; v < RPT; ++v) z[c][v] = __dsub_rn(z[c][v], __dmul_rn(rk[c], qv[v]));
+                    }
+                    if (store) {
+#pragma unroll
+                        for (int c = 0; c < CU; ++c)
+                            if (c0 + c < a.w)
+#pragma unroll
+                                for (int v = 0; v < RPT; ++v)
+                                    if (ok[v]) a.W[(int64_t)(a.c0 + c0 + c) * a.ldw + row0 + (int64_t)v * kBlock] = z[c][v];
                     }
                 }
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {
-                    const int j = a.c0 + c0 + c;
-                    const bool cj = c0 + c < a.w;
-                    const double rj = (cj && upd) ? (a.redundant ? rs[c0 + c] : __ldcg(a.Rt + (int64_t)(k - 1) * a.n + j))
-                                                  : 0.0;
                     acc[c] = 0.0;
 #pragma unroll
-                    for (int v = 0; v < RPT; ++v) {
-                        const int64_t r = row0 + (int64_t)v * kBlock;
-                        if (upd) {
-                            z[c][v] = __dsub_rn(z[c][v], __dmul_rn(rj, q[v]));
-                            if (cj && ok[v]) a.W[(int64_t)j * a.ldw + r] = z[c][v];
-                            if (HP) {
-                                x[c][v] = __dsub_rn(x[c][v], __dmul_rn(rj, pp[v]));
-                                if (cj && ok[v]) a.X[(int64_t)j * a.ldx + r] = x[c][v];
-                            }
-                        }
-                        const double d = CGS ? ((cj && ok[v]) ? __ldcg(a.Z0 + (int64_t)j * a.ldz0 + r) : 0.0) : z[c][v];
-                        acc[c] = fma(p[v], d, acc[c]);
-                    }
+                    for (int v = 0; v < RPT; ++v) acc[c] = fma(p[v], CGS ? d0[CGS ? c : 0][v] : z[c][v], acc[c]);
                 }
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {
@@ -950,6 +1215,7 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
             }
             __syncthreads();
         }
+        if (store) sc = k;
         grid.sync();
         if (a.redundant && k + 1 < a.k1) continue;  // the next step forms these totals
         for (int cc = blockIdx.x; cc < a.w; cc += gridDim.x) {

@@ -4,8 +4,11 @@ The knobs exist only in the experiments build (libaqr_b200_exp.so,
 -DAQR_EXPERIMENTS; the shipped libaqr_b200.so compiles them to their
 defaults) and are read once per process, so each variant runs in a
 subprocess on the experiments build and its factors are compared bitwise
-with the shipped library's: other trailing-pass column widths, the
-unpipelined SpMV step, the separate R-row reduction launch, launches
+with the shipped library's: the HP column loop's two-column trailing pass, the
+unpipelined SpMV step, the windowed trailing passes' write-back period
+(1 = the eager schedule: every pass rewrites the trailing block) and the
+HP X catch-up period (0 = x formed from all finished p columns), the
+separate R-row reduction launch, launches
 without programmatic dependent launch, the materialized copy of Z, the
 column-oriented loop for the col methods (by default they run the
 row-oriented step schedule -- for HP that is also the eagerly updated X
@@ -30,7 +33,7 @@ sys.path.insert(0, {repo!r})
 import paper_1703_10440_b200 as aqr
 from paper_1703_10440_b200 import problems
 ip, ix, dv = problems.laplacian5(700, 460, 1e-2)   # m = 322,000: the 2048-row tile path
-m, n = 700 * 460, 7
+m, n = 700 * 460, 20   # > 2 trailing windows and X catch-ups
 Z = problems.rng(9, 7).standard_normal((n, m)).T
 Zd = torch.from_numpy(np.ascontiguousarray(Z.T)).cuda().t()
 op = aqr.CsrSpdOperator(ip, ix, dv)
@@ -72,8 +75,11 @@ def default_factors(tmp_path_factory):
 
 @pytest.mark.parametrize("knobs", [
     {},
-    {"AQR_TRAIL_VARIANT": "3"},
-    {"AQR_TRAIL_VARIANT": "5"},
+    {"AQR_TRAIL_WIN": "1"},
+    {"AQR_TRAIL_WIN": "2"},
+    {"AQR_TRAIL_WIN": "8"},
+    {"AQR_X_WIN": "0"},
+    {"AQR_X_WIN": "3"},
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},
     {"AQR_TRAIL_CTAS": "8"},
@@ -95,6 +101,6 @@ def test_variant_bitwise_equal_default(default_factors, knobs, tmp_path):
 
 def test_shipped_library_ignores_knobs(default_factors, tmp_path):
     """A stray experiment variable does not change the shipped library's schedule."""
-    got = _run({"AQR_COL_SCHEDULE": "1", "AQR_DEFER": "0", "AQR_TRAIL_VARIANT": "5"}, tmp_path / "s.npz")
+    got = _run({"AQR_COL_SCHEDULE": "1", "AQR_DEFER": "0", "AQR_TRAIL_WIN": "1"}, tmp_path / "s.npz")
     for key in default_factors.files:
         assert np.array_equal(got[key], default_factors[key]), key

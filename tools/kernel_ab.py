@@ -1,29 +1,49 @@
-"""A/B of kernel variants (AQR_TRAIL_VARIANT) on config 2: per-kernel CUDA-event times."""
+"""A/B of schedule knobs: per-slot kernel times of one factorization.
+
+    AQR_LIB_PATH=paper_1703_10440_b200/libaqr_b200_exp.so AQR_TRAIL_WIN=4 \
+        python tools/kernel_ab.py [method] [config 2|5] [reps]
+
+Prints one JSON line: the step time (CUDA events, K factorizations back to
+back) and, from a second pass with the library's kernel timer on, per slot
+(0 trailing pass, 1 fused SpMV step, 2 column update + norm, 3 HP X
+catch-up) the time per factorization, per launch and the algorithmic GB/s.
+"""
 import ctypes, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1703_10440_b200 as aqr
 from paper_1703_10440_b200 import problems, _lib
 L = _lib.lib()
-(ip, ix, dv), Z = problems.config2(device=False)
-op = aqr.CsrSpdOperator(ip, ix, dv)
-Zd = torch.from_numpy(Z.T).cuda().t()
 meth = sys.argv[1] if len(sys.argv) > 1 else "mgs-ha-row"
-for _ in range(3):
-    aqr.factorize(Zd, op, meth)
+cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+K = int(sys.argv[3]) if len(sys.argv) > 3 else (5 if cfg == 2 else 2)
+if cfg == 5:
+    csr, Zd = problems.config5()
+    op = aqr.CsrSpdOperator(*csr)
+    del csr
+else:
+    (ip, ix, dv), Z = problems.config2(device=False)
+    op = aqr.CsrSpdOperator(ip, ix, dv)
+    Zd = torch.from_numpy(Z.T).cuda().t()
+for _ in range(2 if cfg == 5 else 3):
+    r = aqr.factorize(Zd, op, meth)
+    del r
 torch.cuda.synchronize()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-ev0.record(); K = 5
+ev0.record()
 for _ in range(K):
-    aqr.factorize(Zd, op, meth)
+    r = aqr.factorize(Zd, op, meth)
+    del r
 ev1.record(); torch.cuda.synchronize()
 step = ev0.elapsed_time(ev1) / K
 L.aqr_trailing_timer_enable(1)
 for _ in range(K):
-    aqr.factorize(Zd, op, meth)
+    r = aqr.factorize(Zd, op, meth)
+    del r
 torch.cuda.synchronize()
-out = {"variant": os.environ.get("AQR_TRAIL_VARIANT", "0"), "method": meth, "step_ms": step}
-for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update"), (3, "spmv_trail")):
+knobs = {k: v for k, v in os.environ.items() if k.startswith("AQR_")}
+out = {"knobs": knobs, "method": meth, "config": cfg, "step_ms": step}
+for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update"), (3, "x_catchup"), (4, "block_apply")):
     n, ms, b = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
     L.aqr_kernel_timer_read(slot, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b))
     if n.value:
@@ -31,13 +51,3 @@ for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update"), (3, "sp
                      "GBps": b.value / (ms.value / 1e3) / 1e9}
 L.aqr_trailing_timer_enable(0)
 print(json.dumps(out))
-if os.environ.get("AQR_LIST"):
-    import numpy as np
-    L.aqr_trailing_timer_enable(1)
-    aqr.factorize(Zd, op, meth)
-    torch.cuda.synchronize()
-    ms = np.zeros(512); by = np.zeros(512)
-    k = L.aqr_kernel_timer_list(0, ms.ctypes.data, by.ctypes.data, 512)
-    for j in range(k):
-        print(f"launch {j:3d} us {1e3*ms[j]:8.1f} MB {by[j]/1e6:8.1f} GB/s {by[j]/(ms[j]/1e3)/1e9:7.0f} ideal_us {by[j]/6554.9e9*1e6:7.1f}")
-    L.aqr_trailing_timer_enable(0)
