@@ -111,8 +111,8 @@ def config_dict(cfg, method, m, n, nnz, world):
     return d
 
 
-TRAIL_WIN = 6  # write-back period of the windowed trailing passes (AQR_TRAIL_WIN default)
-X_WIN = 8      # HP X catch-up period (AQR_X_WIN default)
+TRAIL_WIN = 4  # write-back period of the windowed trailing passes (AQR_TRAIL_WIN default)
+X_WIN = 16     # HP X catch-up period (AQR_X_WIN default)
 
 
 def survey_bytes(variant, m, n, bytes_A):

@@ -189,6 +189,15 @@ AQR_API aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t o
 AQR_API aqr_status aqr_op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                         int64_t ldy, void *stream);
 
+/* Y = A X as the HP type's block apply runs it (X = op.apply_block(Zw),
+ * gram_schmidt.py:136): dense operators on the FP64 tensor cores (DMMA,
+ * TMA-fed tiles; fused multiply-adds in k-blocks of 4, so the entries differ
+ * from aqr_op_apply's at rounding level), CSR and callback operators exactly
+ * as aqr_op_apply.  Replaces operators.py:58-66 (apply_block) on the HP path
+ * only; aqr_op_apply stays the bitwise kernel-namespace product. */
+AQR_API aqr_status aqr_block_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
+                                   int64_t ldy, void *stream);
+
 /* ---- the reference kernel namespace (backend.kernels()) ---------------- */
 
 /* out[0] = x . y  (deterministic tree reduction; device scalar out)       */

@@ -92,6 +92,7 @@ SIGNATURES = {
                                    c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64),
                                    ctypes.POINTER(c_dbl), c_vp, ctypes.POINTER(c_i64)]),
     "aqr_op_apply": (c_i32, [ctypes.POINTER(AqrOp), c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "aqr_block_apply": (c_i32, [ctypes.POINTER(AqrOp), c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_dot": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "aqr_sub_scaled": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "aqr_div_scalar": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),

@@ -27,6 +27,7 @@
 
 #include "../../include/aqr_b200.h"
 #include "aqr_dense.cuh"
+#include "aqr_dgemm.cuh"
 #include "aqr_kernels.cuh"
 #include "aqr_p2p.cuh"
 
@@ -174,6 +175,8 @@ AQR_KNOB(ldg_reverse_mode, "AQR_LDG_REVERSE", 1)
 // columns per iteration for MGS (default one).
 #ifdef AQR_EXPERIMENTS
 AQR_KNOB(trail_variant, "AQR_TRAIL_VARIANT", 0)
+// AQR_TRAIL_CU=4: the windowed MGS pass with four columns per iteration
+AQR_KNOB(trail_cu, "AQR_TRAIL_CU", 2)
 #endif
 // AQR_SPMV_VARIANT=3: the unpipelined fused SpMV step.
 AQR_KNOB(spmv_variant, "AQR_SPMV_VARIANT", 0)
@@ -191,12 +194,19 @@ AQR_KNOB(defer_mode, "AQR_DEFER", 1)
 AQR_KNOB(spmv_repeat, "AQR_SPMV_REPEAT", 0)
 // AQR_TRAIL_WIN=b: the row form's trailing block is written back every b-th
 // pass (trailing_w_kernel; 1 = every pass, the eager schedule).
-AQR_KNOB(trail_win_knob, "AQR_TRAIL_WIN", 6)
+AQR_KNOB(trail_win_knob, "AQR_TRAIL_WIN", 4)
 int trail_win() { return std::min(std::max(trail_win_knob(), 1), 8); }
 // AQR_X_WIN=b: HP row form, the stored X columns catch up every b steps
 // (0 = never: x_j formed from all j finished p columns).
-AQR_KNOB(x_win_knob, "AQR_X_WIN", 8)
+AQR_KNOB(x_win_knob, "AQR_X_WIN", 16)
 int64_t x_win() { return x_win_knob() > 0 ? x_win_knob() : (int64_t)1 << 40; }
+// AQR_DGEMM=0: the HP block apply of a dense operator in the reference's
+// sequential order (dense_gemm3_kernel) instead of the FP64 tensor cores;
+// 2: the tensor cores for every size (default: operators >= 4096^2 entries).
+AQR_KNOB(dgemm_mode, "AQR_DGEMM", 1)
+// AQR_SPMM_SG=s: long-row SpMM (csr_spmm2_kernel) launch order, s column
+// blocks of 8 per super-group (0: all column blocks of a row block adjacent).
+AQR_KNOB(spmm_sg, "AQR_SPMM_SG", 4)
 // AQR_DEBUG_TIMING=1: host-side enqueue timings on stderr.
 AQR_KNOB(debug_timing, "AQR_DEBUG_TIMING", 0)
 
@@ -266,8 +276,9 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
                       int64_t ldy, const double *qprev, const double *r, double *znew,
                       const aqr::NormOut &out, cudaStream_t s, const aqr::RrowIn *rin = nullptr) {
     aqr::CsrArgs a;
-    std::memset(&a.rin, 0, sizeof a.rin);
+    std::memset(&a, 0, sizeof a);
     a.trace = out.npart != nullptr ? trace_slot() : -1;
+    a.sg = spmm_sg();
     if (rin && out.npart != nullptr) a.rin = *rin;
     a.m = op->m;
     a.k = k;
@@ -331,7 +342,7 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
             launch_pdl(aqr::csr_step_pf_kernel<8, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
         return launched("csr_step_kernel");
     }
-    if (k > 1 && (mr > 8 || mr <= 0)) {  // long (or unknown) rows: CTA = (8 columns, 256 rows)
+    if (k > 1 && (mr > 8 || mr <= 0) && ldx < ((int64_t)1 << 29)) {  // long (or unknown) rows: CTA = (8 columns, 256 rows)
         const int64_t nb = (op->m + aqr::kBlock - 1) / aqr::kBlock;
         aqr::csr_spmm2_kernel<4, 8, 2><<<(unsigned)(((k + 7) / 8) * nb), aqr::kBlock, 0, s>>>(a);
         return launched("csr_spmm2_kernel");
@@ -346,6 +357,72 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         aqr::csr_row_kernel<8><<<(unsigned)grid, aqr::kBlock, 0, s>>>(a);
     return launched("csr_row_kernel");
 }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point table (the
+// library does not link libcuda; nullptr when unavailable).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+    static const EncodeTiledFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+// 2D fp64 tensor map of a column-major rows x cols matrix (ld in elements),
+// box {box_rows, box_cols}, 128-byte swizzle, out-of-bounds zero fill.
+static bool tensor_map_2d(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, int64_t ld,
+                          uint32_t box_rows, uint32_t box_cols) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+    const cuuint32_t box[2] = {box_rows, box_cols};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Y = A X on the FP64 tensor cores (dense_dmma_kernel): the HP block apply
+// of a dense operator.  Returns false (nothing launched) when the operands
+// do not meet TMA's alignment rules.
+// The choice must not depend on k or on which columns X starts at: the
+// host-input pipeline applies the HP block chunk by chunk (X at column c0 of
+// the staged Z) and must produce the bits of the one-call block apply --
+// so the criteria are the operands' base alignment and even leading
+// dimensions (then every column of X is 16-byte aligned), and k = 1 runs
+// on the tensor cores too.
+static bool launch_dense_dmma(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                              cudaStream_t s) {
+    const int64_t m = op->m, K = op->ncols > 0 ? op->ncols : op->m;
+    if (m < 1 || K < 1 || k < 1 || m > INT32_MAX || K > INT32_MAX) return false;
+    // operators below 4096^2 entries keep the sequential product: there the
+    // block apply is a few hundred microseconds at most, and the bits stay
+    // the reference's (HP is sensitive to X's rounding on ill-conditioned
+    // inputs; the golden cases pin it)
+    if (m * K < ((int64_t)1 << 24) && dgemm_mode() != 2) return false;
+    if (op->lda % 2 || ldx % 2 || (uintptr_t)op->A % 16 || (uintptr_t)X % 16) return false;
+    CUtensorMap ta, tx;
+    if (!tensor_map_2d(&ta, op->A, m, K, op->lda, 16, aqr::kDgBK)) return false;
+    if (!tensor_map_2d(&tx, X, K, k, ldx, aqr::kDgBK, aqr::kDgBN)) return false;
+    if (ensure_smem(aqr::dense_dmma_kernel, aqr::kDgSmem) != AQR_OK) return false;
+    const int64_t tiles = ((m + aqr::kDgBM - 1) / aqr::kDgBM) * ((k + aqr::kDgBN - 1) / aqr::kDgBN);
+    aqr::dense_dmma_kernel<<<(unsigned)tiles, aqr::kDgThreads, aqr::kDgSmem, s>>>(ta, tx, m, K, k, Y, ldy);
+    return true;
+}
+
+// HP block apply X = op.apply_block(Zw) (gram_schmidt.py:136) of the
+// factorization: dense operators on the FP64 tensor cores (tolerance-gated
+// rounding), everything else as op_apply.
+aqr_status block_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                       cudaStream_t s);
 
 aqr_status dense_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                        int64_t ldy, cudaStream_t s) {
@@ -384,6 +461,18 @@ aqr_status op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, d
     const aqr_status st = op_apply_impl(op, k, X, ldx, Y, ldy, s);
     timer_end(tix, s);
     return st;
+}
+
+aqr_status block_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                       cudaStream_t s) {
+    if (op && op->kind == AQR_OP_DENSE && k >= 1 && op->A && op->lda >= op->m && dgemm_mode() != 0) {
+        const double abytes = 8.0 * (double)op->m * (double)(op->ncols > 0 ? op->ncols : op->m);
+        const long tix = timer_begin(4, abytes + 16.0 * (double)op->m * (double)k, s);
+        const bool ok = launch_dense_dmma(op, k, X, ldx, Y, ldy, s);
+        timer_end(tix, s);
+        if (ok) return launched("dense_dmma_kernel");
+    }
+    return op_apply(op, k, X, ldx, Y, ldy, s);
 }
 
 aqr_status op_apply_impl(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
@@ -499,7 +588,7 @@ aqr_status launch_x_catchup(int64_t m, double *X, int64_t ldx, int64_t jbeg, int
     a.nk = (int32_t)nk;
     a.status = status;
     const int64_t groups = (jend - jbeg + aqr::kXcCols - 1) / aqr::kXcCols;
-    const int64_t rows = (m + aqr::kBlock - 1) / aqr::kBlock;
+    const int64_t rows = (m + aqr::kBlock * aqr::kXcRows - 1) / (aqr::kBlock * aqr::kXcRows);
     const long tix = timer_begin(3, (double)m * (16.0 * (double)(jend - jbeg) + 8.0 * (double)nk), s);
     launch_pdl(aqr::x_catchup_kernel, dim3((unsigned)(groups * rows)), aqr::kBlock, 0, s, a);
     timer_end(tix, s);
@@ -589,6 +678,9 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
         AQR_TRY(ensure_smem(aqr::trailing_w_kernel<RPT, CU, CGS>, smw));                 \
         launch_pdl(aqr::trailing_w_kernel<RPT, CU, CGS>, grid, aqr::kBlock, smw, s, a); \
     } while (0)
+#ifdef AQR_EXPERIMENTS
+        if (big && !cgs && trail_cu() == 4) { LAUNCHW(8, 4, false); goto done; }
+#endif
         if (big) { if (cgs) LAUNCHW(8, 2, true); else LAUNCHW(8, 2, false); }
         else     { if (cgs) LAUNCHW(1, 4, true); else LAUNCHW(1, 4, false); }
 #undef LAUNCHW
@@ -796,9 +888,10 @@ struct Run {
     // x_j^(j) from them and p_xbase .. p_{j-1} (col_lazy_norm_kernel).
     int64_t xbase = 0;
     // Direct mode (row form, Z distinct from Q): the input Z is read in place
-    // by steps 0 and 1 -- the first writes of the trailing columns happen in
-    // the trailing pass of step 1 -- so the copy Zw = Z (gram_schmidt.py:131)
-    // is never materialized; CGS dots use Z itself as Z0.
+    // until the first write-back pass (column j+1 alone is written by every
+    // pass j >= 1; zread: steps 0 and 1 read their own column from Z), so the
+    // copy Zw = Z (gram_schmidt.py:131) is never materialized; CGS dots use Z
+    // itself as Z0.
     const double *Zin = nullptr;
     int64_t ldzin = 0;
     const double *Z0p = nullptr;
@@ -894,7 +987,7 @@ struct Run {
         if (cgs)
             AQR_CUDA(copy_cols(col(Z0, m, c0), m, col(W, ldw, c0), ldw, m, w, cudaMemcpyDeviceToDevice, s));
         if (hp) {  // X = op.apply_block(Zw), chunk by chunk
-            AQR_TRY(op_apply(a->op, w, col(W, ldw, c0), ldw, col(X, m, c0), m, s));
+            AQR_TRY(block_apply(a->op, w, col(W, ldw, c0), ldw, col(X, m, c0), m, s));
             mv += w;
         }
         // steps 0 .. i-1 in one cooperative launch
@@ -969,6 +1062,9 @@ struct Run {
                                          rt(xbase, j), n, r, xo, norm_out(j), pin, s));
             // every x_win() steps: the stored columns j+1 .. live-1 catch up
             // to x^(j) (R rows < j are final once this step's kernel ran)
+            // (a side-stream form -- the columns needed soon on this stream,
+            // the rest overlapping the next trailing passes -- measured no
+            // faster: 1235-1618 vs 1240 ms on config 5)
             if (j - xbase >= x_win() && j + 1 < live) {
                 AQR_TRY(launch_x_catchup(m, X, m, j + 1, live, pbase() + xbase * m, m, rt(xbase, 0), n, j - xbase,
                                          status, s));
@@ -1295,7 +1391,7 @@ static aqr_status gs_factor_impl(aqr_factor_args *a, void *stream, HostOut *ho, 
     if (r.cgs && !r.pp && !direct)  // Z0, line 132 (per chunk when pipelined)
         AQR_CUDA(copy_cols(r.Z0, m, a->Q, a->ldq, m, n, cudaMemcpyDeviceToDevice, s));
     if (r.hp && !r.pp) {  // X = op.apply_block(Zw), line 136 (per chunk when pipelined)
-        AQR_TRY(op_apply(a->op, n, direct ? a->Z : a->Q, direct ? a->ldz : a->ldq, r.X, m, s));
+        AQR_TRY(block_apply(a->op, n, direct ? a->Z : a->Q, direct ? a->ldz : a->ldq, r.X, m, s));
         r.mv += n;
     }
     const bool dbg_timing = debug_timing() != 0;
@@ -1913,6 +2009,14 @@ aqr_status aqr_op_apply(const aqr_op *op, int64_t k, const double *X, int64_t ld
     if (!op || k < 0 || (k > 1 && ldx < xrows) || ldy < op->m) return set_err(AQR_EARG, "bad apply arguments");
     if (k == 0) return AQR_OK;
     return op_apply(op, k, X, ldx, Y, ldy, S(stream));
+}
+
+aqr_status aqr_block_apply(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y, int64_t ldy,
+                           void *stream) {
+    const int64_t xrows = (op && op->kind == AQR_OP_DENSE && op->ncols > 0) ? op->ncols : (op ? op->m : 0);
+    if (!op || k < 0 || (k > 1 && ldx < xrows) || ldy < op->m) return set_err(AQR_EARG, "bad apply arguments");
+    if (k == 0) return AQR_OK;
+    return block_apply(op, k, X, ldx, Y, ldy, S(stream));
 }
 
 aqr_status aqr_dot(int64_t m, const double *x, const double *y, double *out, void *stream) {

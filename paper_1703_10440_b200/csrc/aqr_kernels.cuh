@@ -558,10 +558,11 @@ __global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
 // projections k = kbeg .. kbeg + nk - 1: x -= r_kj p_k in ascending k with
 // the reference's separately rounded multiply and subtract (gram_schmidt.py:
 // 143-145) -- the same rounding sequence, so the bits of every x_j are
-// unchanged; only where the terms are applied moves.  One thread per row
-// keeps CU columns in registers and streams the p_k of its row; the column
-// groups are the grid's fastest dimension, so the CTAs sharing a row block
-// run together and the p_k rows come from L2 after the first.
+// unchanged; only where the terms are applied moves.  A thread keeps 8
+// columns x 4 rows in registers and streams the p_k of its rows (each r_kj
+// read from shared memory serves 4 updates); the column groups are the
+// grid's fastest dimension, so the CTAs sharing a row block run together
+// and the p_k rows come from L2 after the first.
 struct XCatchArgs {
     int64_t m;
     double *X;
@@ -575,20 +576,25 @@ struct XCatchArgs {
     const int32_t *status;
 };
 constexpr int kXcCols = 8;  // columns per thread
+constexpr int kXcRows = 4;  // rows per thread (each r_kj load serves kXcRows updates)
 constexpr int kXcK = 32;    // r_kj staged per chunk of k
-constexpr int kXcPf = 8;    // p_k loads in flight per thread
-__global__ void __launch_bounds__(kBlock, 4) x_catchup_kernel(XCatchArgs a) {
-    __shared__ double rs[kXcK][kXcCols];
+__global__ void __launch_bounds__(kBlock, 2) x_catchup_kernel(XCatchArgs a) {
+    __shared__ __align__(16) double rs[kXcK][kXcCols];
     pdl_wait();
     if (failed(a.status)) return;
     const int groups = (a.jend - a.jbeg + kXcCols - 1) / kXcCols;  // column groups fastest
-    const int64_t r = (int64_t)(blockIdx.x / groups) * kBlock + threadIdx.x;
-    const bool ok = r < a.m;
+    const int64_t row0 = (int64_t)(blockIdx.x / groups) * (kBlock * kXcRows) + threadIdx.x;
     const int j0 = a.jbeg + (int)(blockIdx.x % groups) * kXcCols;
     const int nc = min(kXcCols, a.jend - j0);
-    double x[kXcCols];
+    bool ok[kXcRows];
 #pragma unroll
-    for (int c = 0; c < kXcCols; ++c) x[c] = (ok && c < nc) ? a.X[(int64_t)(j0 + c) * a.ldx + r] : 0.0;
+    for (int v = 0; v < kXcRows; ++v) ok[v] = row0 + (int64_t)v * kBlock < a.m;
+    double x[kXcCols][kXcRows];
+#pragma unroll
+    for (int c = 0; c < kXcCols; ++c)
+#pragma unroll
+        for (int v = 0; v < kXcRows; ++v)
+            x[c][v] = (ok[v] && c < nc) ? a.X[(int64_t)(j0 + c) * a.ldx + row0 + (int64_t)v * kBlock] : 0.0;
     for (int kc = 0; kc < a.nk; kc += kXcK) {
         const int kn = min(kXcK, a.nk - kc);
         __syncthreads();
@@ -597,16 +603,28 @@ __global__ void __launch_bounds__(kBlock, 4) x_catchup_kernel(XCatchArgs a) {
             rs[k][c] = (k < kn && c < nc) ? __ldg(a.R + (int64_t)(kc + k) * a.rstride + j0 + c) : 0.0;
         }
         __syncthreads();
-        for (int k0 = 0; k0 < kn; k0 += kXcPf) {
-            double pv[kXcPf];
+        for (int k0 = 0; k0 < kn; k0 += 2) {
+            double pv[2][kXcRows];
 #pragma unroll
-            for (int u = 0; u < kXcPf; ++u)
-                pv[u] = (ok && k0 + u < kn) ? a.P[(int64_t)(kc + k0 + u) * a.ldp + r] : 0.0;
+            for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int u = 0; u < kXcPf; ++u) {
+                for (int v = 0; v < kXcRows; ++v)
+                    pv[u][v] = (ok[v] && k0 + u < kn) ? a.P[(int64_t)(kc + k0 + u) * a.ldp + row0 + (int64_t)v * kBlock]
+                                                      : 0.0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
                 if (k0 + u < kn) {
+                    double r[kXcCols];
 #pragma unroll
-                    for (int c = 0; c < kXcCols; ++c) x[c] = __dsub_rn(x[c], __dmul_rn(rs[k0 + u][c], pv[u]));
+                    for (int c = 0; c < kXcCols; c += 2) {
+                        const double2 rr = *reinterpret_cast<const double2 *>(&rs[k0 + u][c]);
+                        r[c] = rr.x;
+                        r[c + 1] = rr.y;
+                    }
+#pragma unroll
+                    for (int c = 0; c < kXcCols; ++c)
+#pragma unroll
+                        for (int v = 0; v < kXcRows; ++v) x[c][v] = __dsub_rn(x[c][v], __dmul_rn(r[c], pv[u][v]));
                 }
             }
         }
@@ -614,7 +632,9 @@ __global__ void __launch_bounds__(kBlock, 4) x_catchup_kernel(XCatchArgs a) {
     pdl_trigger();
 #pragma unroll
     for (int c = 0; c < kXcCols; ++c)
-        if (ok && c < nc) a.X[(int64_t)(j0 + c) * a.ldx + r] = x[c];
+#pragma unroll
+        for (int v = 0; v < kXcRows; ++v)
+            if (ok[v] && c < nc) a.X[(int64_t)(j0 + c) * a.ldx + row0 + (int64_t)v * kBlock] = x[c][v];
 }
 
 // Standalone totals of the norm partials (step API / multi-GPU driver).
@@ -1345,6 +1365,7 @@ struct CsrArgs {
     NormOut out;      // out.npart == nullptr: plain apply
     RrowIn rin;       // fused step: deferred r-row totals (partial == nullptr: none)
     int32_t trace;    // AQR_TRACE builds: launch slot (-1 off)
+    int32_t sg;       // csr_spmm2_kernel: column blocks per super-group (0: all)
 };
 
 // sum_q data[q] * xe(indices[q]) over q in [s, e), xe = x - rj qprev (upd),
@@ -1423,38 +1444,70 @@ __device__ __forceinline__ void csr_rows(const CsrArgs &a, const int (&s)[R], co
 // entries in L2; thread = (row, K columns): each batch of B entries is loaded
 // once for K columns (B x K gathers in flight).  Stored-order sums per output
 // as csr_row.  Config 5 block apply: 316 ms (per-column rows) -> 102-117 ms.
+//
+// Launch order (a.sg column blocks per super-group; 0: one super-group):
+// super-group slowest, then row block, then the super-group's column blocks.
+// The CSR rows are read from HBM once per super-group (the column blocks of
+// a row block share them in L2), and the rows of X a super-group gathers
+// -- for a 3-D stencil three grid planes of each of its columns around the
+// advancing row front -- stay in L2 until every row that needs them has
+// run, so X is read about once instead of once per neighbouring plane.
 template <int B, int K, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) csr_spmm2_kernel(CsrArgs a) {
-    const int64_t ncb = (a.k + K - 1) / K;  // 1-D grid: column block fastest
-    const int64_t row = (int64_t)(blockIdx.x / ncb) * kBlock + threadIdx.x;
-    const int64_t col0 = (int64_t)(blockIdx.x % ncb) * K;
+    const int64_t ncb = (a.k + K - 1) / K;
+    const int64_t nrb = (a.m + kBlock - 1) / kBlock;
+    const int64_t sg = (a.sg > 0 && a.sg < ncb) ? a.sg : ncb;  // column blocks per super-group
+    const int64_t per_sg = sg * nrb;                           // CTAs per (full) super-group
+    const int64_t g = blockIdx.x / per_sg, rest = blockIdx.x - g * per_sg;
+    const int64_t w = min(sg, ncb - g * sg);                   // column blocks in this super-group
+    const int64_t rb = rest / w, cb = g * sg + rest % w;
+    const int64_t row = rb * kBlock + threadIdx.x;
+    const int64_t col0 = cb * K;
     if (row >= a.m) return;
     const int s = __ldg(a.indptr + row);
     const int e = __ldg(a.indptr + row + 1);
     double acc[K];
 #pragma unroll
     for (int kk = 0; kk < K; ++kk) acc[kk] = 0.0;
-    for (int q0 = s; q0 < e; q0 += B) {
+    // gather addresses: X + c + (col0 + kk) ldx, formed as one wide
+    // multiply-add per gather from the entry's column-block base (a clamped
+    // column re-reads the block's first column; its sums are not stored)
+    const double *xb = a.X + col0 * a.ldx;
+    const uint32_t cstride = (uint32_t)(a.ldx * 8);  // bytes between columns (host checks < 2^32 / K)
+    uint32_t coff[K];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) coff[kk] = (col0 + kk < a.k ? (uint32_t)kk : 0u);
+    auto gat = [&](int c, int kk) {
+        const char *p = reinterpret_cast<const char *>(xb + c);
+        return __ldg(reinterpret_cast<const double *>(p + (uint64_t)coff[kk] * cstride));
+    };
+    int q0 = s;
+    for (; q0 + B <= e; q0 += B) {  // full batches: no predicates
         int c[B];
         double v[B];
 #pragma unroll
         for (int h = 0; h < B; ++h) {
-            const bool ok = q0 + h < e;
-            c[h] = ok ? __ldg(a.indices + q0 + h) : 0;
-            v[h] = ok ? __ldg(a.data + q0 + h) : 0.0;
+            c[h] = __ldg(a.indices + q0 + h);
+            v[h] = __ldg(a.data + q0 + h);
         }
         double xv[K][B];
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-            const double *x = a.X + (col0 + kk < a.k ? col0 + kk : 0) * a.ldx;
+        for (int kk = 0; kk < K; ++kk)
 #pragma unroll
-            for (int h = 0; h < B; ++h) xv[kk][h] = (q0 + h < e) ? __ldg(x + c[h]) : 0.0;
-        }
+            for (int h = 0; h < B; ++h) xv[kk][h] = gat(c[h], kk);
 #pragma unroll
         for (int kk = 0; kk < K; ++kk)
 #pragma unroll
-            for (int h = 0; h < B; ++h)
-                if (q0 + h < e) acc[kk] = __dadd_rn(acc[kk], __dmul_rn(v[h], xv[kk][h]));
+            for (int h = 0; h < B; ++h) acc[kk] = __dadd_rn(acc[kk], __dmul_rn(v[h], xv[kk][h]));
+    }
+    for (; q0 < e; ++q0) {  // the rest, one entry at a time (stored order)
+        const int c = __ldg(a.indices + q0);
+        const double v = __ldg(a.data + q0);
+        double xv[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) xv[kk] = gat(c, kk);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) acc[kk] = __dadd_rn(acc[kk], __dmul_rn(v, xv[kk]));
     }
 #pragma unroll
     for (int kk = 0; kk < K; ++kk)

@@ -289,9 +289,11 @@ class DistDenseSpdOperator(SpdOperator):
         if self.local_apply is not None:
             return self.local_apply(self, full, k)
         Y = D.empty_f(self.dim, k, full.device)
-        _lib.check(_lib.lib().aqr_op_apply(ctypes.byref(self._native()), k, full.data_ptr(),
+        # k > 1: the HP block apply (FP64 tensor cores); k = 1: the bitwise GEMV
+        fn = "aqr_block_apply" if k > 1 else "aqr_op_apply"
+        _lib.check(getattr(_lib.lib(), fn)(ctypes.byref(self._native()), k, full.data_ptr(),
                                            self.global_dim, Y.data_ptr(), self.dim,
-                                           D.stream_ptr()), "aqr_op_apply")
+                                           D.stream_ptr()), fn)
         return Y
 
     def apply(self, x):

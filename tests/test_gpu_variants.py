@@ -80,6 +80,7 @@ def default_factors(tmp_path_factory):
     {"AQR_TRAIL_WIN": "8"},
     {"AQR_X_WIN": "0"},
     {"AQR_X_WIN": "3"},
+    {"AQR_SPMM_SG": "0"},
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},
     {"AQR_TRAIL_CTAS": "8"},
