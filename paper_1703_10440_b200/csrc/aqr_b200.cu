@@ -207,6 +207,10 @@ AQR_KNOB(dgemm_mode, "AQR_DGEMM", 1)
 // AQR_SPMM_SG=s: long-row SpMM (csr_spmm2_kernel) launch order, s column
 // blocks of 8 per super-group (0: all column blocks of a row block adjacent).
 AQR_KNOB(spmm_sg, "AQR_SPMM_SG", 4)
+// AQR_XC_ROWS=r: rows per thread of the X catch-up (1, 2 or 4; CTAs/SM 6 / 4 / 2;
+// config 5 HP catch-up 187 / 160 / 174 ms, profiles/r02/ab_xc_spmm.jsonl).
+AQR_KNOB(xc_rows_knob, "AQR_XC_ROWS", 2)
+int xc_rows() { const int r = xc_rows_knob(); return (r == 1 || r == 4) ? r : 2; }
 // AQR_DEBUG_TIMING=1: host-side enqueue timings on stderr.
 AQR_KNOB(debug_timing, "AQR_DEBUG_TIMING", 0)
 
@@ -344,6 +348,8 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
     }
     if (k > 1 && (mr > 8 || mr <= 0) && ldx < ((int64_t)1 << 29)) {  // long (or unknown) rows: CTA = (8 columns, 256 rows)
         const int64_t nb = (op->m + aqr::kBlock - 1) / aqr::kBlock;
+        // (batch, columns, CTAs/SM) = (4, 8, 2); (4, 4, 4) / (2, 8, 3) / (8, 4, 3)
+        // measured 115.6 / 85.3 / 114.4 vs 87.5 ms on config 5 (profiles/r02/ab_xc_spmm.jsonl)
         aqr::csr_spmm2_kernel<4, 8, 2><<<(unsigned)(((k + 7) / 8) * nb), aqr::kBlock, 0, s>>>(a);
         return launched("csr_spmm2_kernel");
     }
@@ -588,9 +594,15 @@ aqr_status launch_x_catchup(int64_t m, double *X, int64_t ldx, int64_t jbeg, int
     a.nk = (int32_t)nk;
     a.status = status;
     const int64_t groups = (jend - jbeg + aqr::kXcCols - 1) / aqr::kXcCols;
-    const int64_t rows = (m + aqr::kBlock * aqr::kXcRows - 1) / (aqr::kBlock * aqr::kXcRows);
+    const int rpt = xc_rows();
+    const int64_t rows = (m + aqr::kBlock * rpt - 1) / (aqr::kBlock * rpt);
     const long tix = timer_begin(3, (double)m * (16.0 * (double)(jend - jbeg) + 8.0 * (double)nk), s);
-    launch_pdl(aqr::x_catchup_kernel, dim3((unsigned)(groups * rows)), aqr::kBlock, 0, s, a);
+    if (rpt == 4)
+        launch_pdl(aqr::x_catchup_kernel<4, 2>, dim3((unsigned)(groups * rows)), aqr::kBlock, 0, s, a);
+    else if (rpt == 1)
+        launch_pdl(aqr::x_catchup_kernel<1, 6>, dim3((unsigned)(groups * rows)), aqr::kBlock, 0, s, a);
+    else
+        launch_pdl(aqr::x_catchup_kernel<2, 4>, dim3((unsigned)(groups * rows)), aqr::kBlock, 0, s, a);
     timer_end(tix, s);
     return launched("x_catchup_kernel");
 }

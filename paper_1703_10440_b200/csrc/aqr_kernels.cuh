@@ -576,9 +576,10 @@ struct XCatchArgs {
     const int32_t *status;
 };
 constexpr int kXcCols = 8;  // columns per thread
-constexpr int kXcRows = 4;  // rows per thread (each r_kj load serves kXcRows updates)
 constexpr int kXcK = 32;    // r_kj staged per chunk of k
-__global__ void __launch_bounds__(kBlock, 2) x_catchup_kernel(XCatchArgs a) {
+// kXcRows rows per thread (each r_kj load serves kXcRows updates), MINB CTAs per SM
+template <int kXcRows, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) x_catchup_kernel(XCatchArgs a) {
     __shared__ __align__(16) double rs[kXcK][kXcCols];
     pdl_wait();
     if (failed(a.status)) return;
