@@ -622,7 +622,7 @@ def run_b200_distributed(args, rank, world, local_rank):
     gathered = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
     dist.all_gather(gathered, per_rank)
     bytes_A = 12 * 449_455_096 + 4 * (m + 1)
-    sb = survey_bytes("hp", m, n, bytes_A)  # the peer-memory path runs the eager schedule
+    sb = step_bytes("hp", m, n, bytes_A)  # the whole job: the ranks' row blocks of the same schedule
     step_gbs = sb / (ms_per_step / 1e3) / 1e9
     e2e = None
     if not args.no_e2e:

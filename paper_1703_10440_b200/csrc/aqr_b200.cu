@@ -102,7 +102,8 @@ aqr_status ensure_smem(K kernel, size_t bytes) {
 
 // ---- kernel timer (bench.py's roofline leg) ---------------------------------
 // Slot 0: fused trailing pass; slot 1: fused SpMV step; slot 2: column
-// update + norm; slot 3: HP X catch-up; slot 4: block apply (k > 1).  When enabled, a CUDA event pair is recorded around every
+// update + norm; slot 3: HP X catch-up; slot 4: block apply (k > 1); slot 5:
+// catch-up of a host-pipeline chunk.  When enabled, a CUDA event pair is recorded around every
 // launch of those kernels on the launching stream.
 struct KernelTimer {
     struct Rec {
@@ -1002,8 +1003,9 @@ struct Run {
             AQR_TRY(block_apply(a->op, w, col(W, ldw, c0), ldw, col(X, m, c0), m, s));
             mv += w;
         }
-        // steps 0 .. i-1 in one cooperative launch
-        if (i > 0 && catchup_mode() != 0) {
+        // steps 0 .. i-1 in one cooperative launch (chunks of <= 512 columns:
+        // the kernel keeps a tile's warp totals of every column in shared memory)
+        if (i > 0 && catchup_mode() != 0 && w <= 512) {
             aqr::CatchArgs c;
             std::memset(&c, 0, sizeof c);
             c.m = m;
@@ -1022,12 +1024,16 @@ struct Run {
             c.partial = pp->partial2;
             c.status = status;
             c.trace = trace_slot();
-            // one barrier per step when the totals fit in shared memory
-            // (partial2 holds two parity buffers of the widest chunk)
-            c.redundant = (catchup_mode() != 2 && w <= 4096) ? 1 : 0;
-            // windowed (the r rows of the window in shared memory) for chunks of <= 512 columns
-            c.win = w <= 512 ? trail_win() : 1;
+            // one barrier per step, every CTA forming the previous step's
+            // totals itself, while that costs at most 128 loads per thread
+            // (partial2 holds two parity buffers of the widest chunk); above
+            // (config 5: 16 columns x 8192 tiles) w CTAs form them between two
+            // barriers
+            c.redundant = (catchup_mode() != 2 && (int64_t)w * c.ntiles <= 128 * aqr::kBlock) ? 1 : 0;
+            c.win = trail_win();
+            const long tix = timer_begin(5, 0.0, s);  // (time only)
             AQR_TRY(launch_catchup(c, cgs, s));
+            timer_end(tix, s);
             live = c1;
             zbase = i - 1;  // the chunk holds z^(i-1): projection i-1 is left to step i
             return x_chunk(i, c0, c1);
@@ -1214,7 +1220,9 @@ struct Run {
     }
 };
 
-template <bool HP, bool CGS>
+// Peer-memory trailing pass of step i (windowed Z-only pass for HA and for
+// HP with lazy x, as the single-GPU row form).
+template <bool CGS>
 aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, int64_t i, double *rii,
                                int32_t *status, cudaStream_t s) {
     aqr::TrailArgs a = a0;
@@ -1222,15 +1230,16 @@ aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, 
     a.cpg = choose_cpg_generic(a.ntiles, ncols);
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
-    const size_t smem = sizeof(double) * aqr::kWarps * (size_t)std::max(a.cpg, 1);
-    const long tix = timer_begin(0, trailing_bytes(a, HP, CGS, false), s);
-    if (aqr::rows_per_thread(a.m) == 8) {
-        constexpr int CU = (HP && !CGS) ? 1 : 2;  // as launch_trailing: MGS-HP one column per iteration
-        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, CU, HP, CGS>, smem));
-        launch_pdl(aqr::p2p_trailing_kernel<8, CU, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
+    const bool big = aqr::rows_per_thread(a.m) == 8;
+    const size_t smem = aqr::trail_w_smem(big ? 8 : 1, std::max(a.cpg, 1), a.win);
+    if (a.win > 0) a.qprev = a.qwin + (int64_t)(a.win - 1) * a.ldw;  // trail_prefetch
+    const long tix = timer_begin(0, trailing_bytes(a, false, CGS, true), s);
+    if (big) {
+        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, 2, false, CGS, true>, smem));
+        launch_pdl(aqr::p2p_trailing_kernel<8, 2, false, CGS, true>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
     } else {
-        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, smem));
-        launch_pdl(aqr::p2p_trailing_kernel<1, 4, HP, CGS>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
+        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<1, 4, false, CGS, true>, smem));
+        launch_pdl(aqr::p2p_trailing_kernel<1, 4, false, CGS, true>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
     }
     timer_end(tix, s);
     return launched("p2p_trailing_kernel");
@@ -1461,6 +1470,15 @@ int pipe_sched_mode() { return knob("AQR_PIPE_SCHED", 0); }  // read per call
 std::vector<int64_t> pipe_bounds(int64_t n, int64_t chunk_cols) {
     std::vector<int64_t> b{0};
     if (n <= 0) return b;
+    if (chunk_cols < 0) {  // doubling: w0, w0, 2 w0, 4 w0, ... (w0 = -chunk_cols)
+        int64_t c = 0, w = -chunk_cols;
+        b.push_back(c = std::min(n, w));
+        while (c < n) {
+            b.push_back(c = std::min(n, c + w));
+            w *= 2;
+        }
+        return b;
+    }
     const int sched = chunk_cols > 0 ? 0 : pipe_sched_mode();
     const int64_t w = chunk_cols > 0 ? chunk_cols : std::max<int64_t>(1, (n + 7) / 8);
     int64_t c = 0;
@@ -1673,6 +1691,8 @@ struct P2PRun {
     aqr::P2PArgs P;
     aqr::CsrArgs c;
     std::vector<int32_t> st;
+    // as Run: stored trailing columns at z^(zbase); HP's stored X at x^(xbase)
+    int64_t zbase = 0, xbase = 0;
 
     double *col(double *B, int64_t ld, int64_t j) const { return B + j * ld; }
 
@@ -1781,18 +1801,31 @@ struct P2PRun {
         o.step = i;
         o.status = status;
         const unsigned gn = (unsigned)aqr::norm_tiles(m, hp);
-        if (hp) {
+        if (hp) {  // lazy x: X_i at x^(xbase), p_k in X's column k (k < i)
             aqr::ColArgs ca;
             std::memset(&ca, 0, sizeof ca);
             ca.m = m;
             ca.z = col(W, ldw, i);
             ca.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
             ca.x = col(X, m, i);
-            ca.pprev = i > 0 ? pring + ((i - 1) & 1) * m : nullptr;
+            ca.P = col(X, m, xbase);
+            ca.ldp = m;
+            ca.rcol = Rt + xbase * n + i;
+            ca.rstride = n;
+            ca.nprev = (int32_t)(i - xbase);
+            ca.xout = pring + (i & 1) * m;
             ca.out = o;
             ca.trace = -1;
-            launch_pdl(aqr::p2p_col_update_kernel, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
-            return launched("p2p_col_update_kernel");
+            launch_pdl(aqr::p2p_col_lazy_kernel, gn, aqr::kBlock, 0, s, ca, P, i, Rt);
+            AQR_TRY(launched("p2p_col_lazy_kernel"));
+            // every x_win() steps the stored X columns i+1 .. n-1 catch up
+            // (local rows; R rows < i are final once this kernel ran)
+            if (i - xbase >= x_win() && i + 1 < n) {
+                AQR_TRY(launch_x_catchup(m, X, m, i + 1, n, col(X, m, xbase), m, Rt + xbase * n, n, i - xbase,
+                                         status, s));
+                xbase = i;
+            }
+            return AQR_OK;
         }
         aqr::CsrArgs ca = c;
         ca.k = 1;
@@ -1825,22 +1858,27 @@ struct P2PRun {
         t.ldx = m;
         t.Z0 = Z0;
         t.ldz0 = m;
-        t.qprev = i > 0 ? col(W, ldw, i - 1) : nullptr;
-        t.pprev = (hp && i > 0) ? pring + ((i - 1) & 1) * m : nullptr;
-        t.rprev = i > 0 ? Rt + (i - 1) * n : nullptr;
-        t.psrc = hp ? col(X, m, i) : xvec;
+        // windowed: projections zbase .. i-1 applied in registers, the block
+        // written back every trail_win()-th pass (column i+1 by every pass
+        // with a window: the next step's SpMV halo reads it on the peers)
+        t.win = t.jend > t.jbeg ? (int32_t)(i - zbase) : 0;
+        t.store_all = t.win >= trail_win() ? 1 : 0;
+        t.qwin = t.win > 0 ? col(W, ldw, zbase) : nullptr;
+        t.rwin = t.win > 0 ? Rt + zbase * n : nullptr;
+        t.rstride = n;
+        t.psrc = hp ? pring + (i & 1) * m : xvec;
         t.zsrc = hp ? col(W, ldw, i) : zvec;
         t.qout = col(W, ldw, i);
-        t.pout = hp ? pring + (i & 1) * m : nullptr;
+        t.pout = hp ? col(X, m, i) : nullptr;  // p_i kept for the lazy x of later steps
         t.partial = partial;
         t.status = status;
         t.trace = -1;
         t.reverse = (int32_t)(i & 1);  // backwards on odd steps (L2 reuse, as the single-GPU pass)
         double *rii = Rt + i * n + i;
-        if (hp) return cgs ? launch_p2p_trailing<true, true>(t, P, i, rii, status, s)
-                           : launch_p2p_trailing<true, false>(t, P, i, rii, status, s);
-        return cgs ? launch_p2p_trailing<false, true>(t, P, i, rii, status, s)
-                   : launch_p2p_trailing<false, false>(t, P, i, rii, status, s);
+        const aqr_status st = cgs ? launch_p2p_trailing<true>(t, P, i, rii, status, s)
+                                  : launch_p2p_trailing<false>(t, P, i, rii, status, s);
+        if (t.store_all) zbase = i;
+        return st;
     }
 
     // Step i, third launch: this rank's R-row totals -> every rank.

@@ -464,19 +464,14 @@ __global__ void __launch_bounds__(kBlock, 4) col_update_norm_kernel(ColArgs a) {
 constexpr int kLazyBlk = 4;    // owned 256-row blocks per load batch
 constexpr int kLazyK = 4;      // p columns per batch of loads
 constexpr int kLazyRs = 1024;  // r_{k,j} staged in shared memory per chunk
-__global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
-    trace_mark(a.trace, 0);
-    pdl_wait();
-    trace_mark(a.trace, 1);
-    if (failed(a.out.status)) return;
+// The body: x_j formed, z_j's deferred update (rj), x_j -> a.xout, the
+// thread's norm chains (t, zz, xx) returned.  All kBlock threads.
+__device__ __forceinline__ void col_lazy_body(const ColArgs &a, double rj, bool upd, double &t, double &zz,
+                                              double &xx) {
     __shared__ double rs[kLazyRs];
     const int32_t nk = a.nprev;  // lazy terms k = j - nk .. j-1 (X_j holds x_j^(j - nk))
-    const bool upd = a.r != nullptr || a.rin.partial != nullptr;  // z_j's deferred r_{j-1,j} q_{j-1}
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
     const int64_t G = gridDim.x;
-    // r_{j-1,j}: this kernel forms it from the trailing partials (RrowIn; CTA
-    // 0 stores it to R) or it is already final in R
-    const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
     auto stage = [&](int kc, int kn) {
         for (int k = threadIdx.x; k < kn; k += kBlock)
             rs[k] = (kc + k == nk - 1 && upd) ? rj : __ldcg(a.rcol + (int64_t)(kc + k) * a.rstride);
@@ -484,7 +479,7 @@ __global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
     const bool one_chunk = nk <= kLazyRs;
     if (one_chunk) stage(0, nk);
     __syncthreads();
-    double t = 0.0, zz = 0.0, xx = 0.0;
+    t = zz = xx = 0.0;
     for (int64_t b0 = blockIdx.x; b0 < nblk; b0 += G * kLazyBlk) {
         int64_t row[kLazyBlk];
         bool ok[kLazyBlk];
@@ -544,6 +539,19 @@ __global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(kBlock, 4) col_lazy_norm_kernel(ColArgs a) {
+    trace_mark(a.trace, 0);
+    pdl_wait();
+    trace_mark(a.trace, 1);
+    if (failed(a.out.status)) return;
+    const bool upd = a.r != nullptr || a.rin.partial != nullptr;  // z_j's deferred r_{j-1,j} q_{j-1}
+    // r_{j-1,j}: this kernel forms it from the trailing partials (RrowIn; CTA
+    // 0 stores it to R) or it is already final in R
+    const double rj = a.rin.partial ? rrow_first(a.rin, blockIdx.x == 0) : (upd ? *a.r : 0.0);
+    double t, zz, xx;
+    col_lazy_body(a, rj, upd, t, zz, xx);
     pdl_trigger();
     norm_cta_partial(a.out, t, zz, xx, blockIdx.x);
     norm_last_cta(a.out, gridDim.x);
@@ -1080,11 +1088,12 @@ struct CatchArgs {
     int32_t win;        // write-back period (1: every step)
 };
 
-// Dynamic shared memory: wsum [kWarps][2], rs [wpad] (redundant totals),
-// rsm [win][wpad] (the window's r rows), qs [win][RPT][kBlock].
+// Dynamic shared memory: wsum [kWarps][wpad] (warp totals of a tile's
+// units), rs [wpad] (redundant totals), rsm [win][wpad] (the window's r
+// rows), qs [win][RPT][kBlock].
 __host__ __device__ inline int catch_wpad(int w) { return ((w + 7) / 8) * 8; }
 __host__ __device__ inline size_t catch_smem(int rpt, int w, int win, bool redundant) {
-    return sizeof(double) * ((size_t)2 * kWarps + (redundant ? catch_wpad(w) : 0) +
+    return sizeof(double) * ((size_t)kWarps * catch_wpad(w) + (redundant ? catch_wpad(w) : 0) +
                              (size_t)win * catch_wpad(w) + (size_t)win * rpt * kBlock);
 }
 
@@ -1107,7 +1116,7 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
     extern __shared__ double smc[];
     const int wpad = catch_wpad(a.w);
     double *wsum = smc;
-    double *rs = wsum + 2 * kWarps;
+    double *rs = wsum + kWarps * wpad;
     double *rsm = rs + (a.redundant ? wpad : 0);
     double *qs = rsm + a.win * wpad;
     __shared__ double tot1[1];
@@ -1149,36 +1158,40 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
         const int ng = (a.w + CU - 1) / CU;
         const int64_t U = (int64_t)a.ntiles * ng;
         const int64_t ub = U * blockIdx.x / gridDim.x, ue = U * (blockIdx.x + 1) / gridDim.x;
-        int cur = -1;
         double p[RPT];
         bool ok[RPT];
-        // odd steps walk the range backwards: a step starts on the units the
-        // previous one touched last (still in L2); per unit independent, so
-        // the bits do not depend on the walk
+        // The range is walked tile by tile: the step vectors and the q window
+        // load once per tile, the tile's units keep their warp totals in
+        // wsum[warp][column] (no barrier between units, so the loads of the
+        // next unit are not held back), and one pair of barriers per tile
+        // turns them into the tile's partials.  Odd steps walk the tiles
+        // backwards: a step starts on the tiles the previous one touched last
+        // (still in L2); per unit independent, so the bits do not depend on
+        // the walk.
         const bool back = AQR_CATCHUP_REVERSE && (k & 1);
-        for (int64_t uu = ub; uu < ue; ++uu) {
-            const int64_t u = back ? ub + ue - 1 - uu : uu;
-            const int tile = (int)(u / ng), c0 = (int)(u % ng) * CU;
+        const int t_lo = (int)(ub / ng), t_hi = ue > ub ? (int)((ue - 1) / ng) : t_lo - 1;
+        for (int ti = t_lo; ti <= t_hi; ++ti) {
+            const int tile = back ? t_lo + t_hi - ti : ti;
+            const int g0 = (int)(ub > (int64_t)tile * ng ? ub - (int64_t)tile * ng : 0);       // first unit of the tile
+            const int g1 = (int)(ue < (int64_t)(tile + 1) * ng ? ue - (int64_t)tile * ng : ng);  // one past the last
             const int64_t row0 = (int64_t)tile * (kBlock * RPT) + threadIdx.x;
-            if (tile != cur) {  // thread-private rows: no barrier needed
-                cur = tile;
 #pragma unroll
-                for (int v = 0; v < RPT; ++v) {
-                    const int64_t r = row0 + (int64_t)v * kBlock;
-                    ok[v] = r < a.m;
-                    const double ps = ok[v] ? __ldcg(psrc + r) : 0.0;
-                    p[v] = a.p_direct ? ps : ps / rii;
-                }
-                for (int kk = 0; kk < win; ++kk) {
-                    double qv[RPT];
-#pragma unroll
-                    for (int v = 0; v < RPT; ++v)
-                        qv[v] = ok[v] ? __ldcg(a.W + (int64_t)(sc + kk) * a.ldw + row0 + (int64_t)v * kBlock) : 0.0;
-#pragma unroll
-                    for (int v = 0; v < RPT; ++v) qs[(kk * RPT + v) * kBlock + threadIdx.x] = qv[v];
-                }
+            for (int v = 0; v < RPT; ++v) {  // thread-private rows: no barrier needed
+                const int64_t r = row0 + (int64_t)v * kBlock;
+                ok[v] = r < a.m;
+                const double ps = ok[v] ? __ldcg(psrc + r) : 0.0;
+                p[v] = a.p_direct ? ps : ps / rii;
             }
-            {
+            for (int kk = 0; kk < win; ++kk) {
+                double qv[RPT];
+#pragma unroll
+                for (int v = 0; v < RPT; ++v)
+                    qv[v] = ok[v] ? __ldcg(a.W + (int64_t)(sc + kk) * a.ldw + row0 + (int64_t)v * kBlock) : 0.0;
+#pragma unroll
+                for (int v = 0; v < RPT; ++v) qs[(kk * RPT + v) * kBlock + threadIdx.x] = qv[v];
+            }
+            for (int g = g0; g < g1; ++g) {
+                const int c0 = g * CU;
                 const bool needz = !CGS || store;
                 double z[CU][RPT], d0[CGS ? CU : 1][RPT], acc[CU];
 #pragma unroll
@@ -1223,16 +1236,15 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {
                     const double sw = warp_sum(acc[c]);
-                    if (lane == 0) wsum[warp * CU + c] = sw;
+                    if (lane == 0 && c0 + c < a.w) wsum[warp * wpad + c0 + c] = sw;
                 }
             }
             __syncthreads();
-            if (threadIdx.x < CU && c0 + (int)threadIdx.x < a.w) {
-                const int c = threadIdx.x;
+            for (int c = g0 * CU + threadIdx.x; c < min(g1 * CU, a.w); c += kBlock) {
                 double s = wsum[c];
 #pragma unroll
-                for (int w2 = 1; w2 < kWarps; ++w2) s = __dadd_rn(s, wsum[w2 * CU + c]);
-                part[(int64_t)(c0 + c) * a.ntiles + tile] = s;
+                for (int w2 = 1; w2 < kWarps; ++w2) s = __dadd_rn(s, wsum[w2 * wpad + c]);
+                part[(int64_t)c * a.ntiles + tile] = s;
             }
             __syncthreads();
         }

@@ -260,52 +260,23 @@ __global__ void __launch_bounds__(kBlock, 3) p2p_csr_step_kernel(CsrArgs a, P2PA
     p2p_norm_out(p, a.out, gridDim.x, i);
 }
 
-// HP column update (z_i, x_i) + norm partials, as col_update_norm_kernel.
-__global__ void __launch_bounds__(kBlock, 4) p2p_col_update_kernel(ColArgs a, P2PArgs p, int64_t i, double *Rt) {
+// HP, lazy x (as col_lazy_norm_kernel): r_{i-1,i} and row i-1 of R from the
+// exchanged R rows, x_i formed from the stored X_i and the p window, the
+// deferred z_i update, the norm partials -> every rank.
+__global__ void __launch_bounds__(kBlock, 4) p2p_col_lazy_kernel(ColArgs a, P2PArgs p, int64_t i, double *Rt) {
     pdl_wait();
     if (failed(a.out.status)) return;
-    const bool upd = i > 0;
     const double rj = p2p_rrow_in(p, i, Rt);
-    const int64_t nblk = (a.m + kBlock - 1) / kBlock;
-    const int64_t G = gridDim.x;
-    double t = 0.0, zz = 0.0, xx = 0.0;
-    for (int64_t b0 = blockIdx.x; b0 < nblk; b0 += G * kColTiles) {
-        double z[kColTiles], xv[kColTiles], q[kColTiles], pp[kColTiles];
-#pragma unroll
-        for (int g = 0; g < kColTiles; ++g) {
-            const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
-            const bool ok = b0 + g * G < nblk && r < a.m;
-            z[g] = ok ? a.z[r] : 0.0;
-            q[g] = (ok && upd) ? a.qprev[r] : 0.0;
-            xv[g] = ok ? a.x[r] : 0.0;
-            pp[g] = (ok && upd) ? a.pprev[r] : 0.0;
-        }
-#pragma unroll
-        for (int g = 0; g < kColTiles; ++g) {
-            const int64_t r = (b0 + g * G) * kBlock + threadIdx.x;
-            const bool ok = b0 + g * G < nblk && r < a.m;
-            if (upd) {
-                z[g] = __dsub_rn(z[g], __dmul_rn(rj, q[g]));
-                xv[g] = __dsub_rn(xv[g], __dmul_rn(rj, pp[g]));
-                if (ok) {
-                    a.z[r] = z[g];
-                    a.x[r] = xv[g];
-                }
-            }
-            if (ok) {
-                t = fma(z[g], xv[g], t);
-                zz = fma(z[g], z[g], zz);
-                xx = fma(xv[g], xv[g], xx);
-            }
-        }
-    }
+    double t, zz, xx;
+    col_lazy_body(a, rj, i > 0, t, zz, xx);
     norm_cta_partial(a.out, t, zz, xx, blockIdx.x);
     p2p_norm_out(p, a.out, gridDim.x, i);
 }
 
 // Trailing pass of step i: global norm totals (rank-ordered) -> r_ii, the
-// breakdown / flag record (CTA 0), then the pass over the local rows.
-template <int RPT, int CU, bool HP, bool CGS>
+// breakdown / flag record (CTA 0), then the pass over the local rows
+// (WIN: the windowed Z-only pass, trail_body_w).
+template <int RPT, int CU, bool HP, bool CGS, bool WIN>
 __global__ void __launch_bounds__(kBlock) p2p_trailing_kernel(TrailArgs a, P2PArgs p, int64_t i, double *rii_out,
                                                               int32_t *status) {
     // as trailing_kernel: odd steps walk the units backwards, and this
@@ -332,7 +303,10 @@ __global__ void __launch_bounds__(kBlock) p2p_trailing_kernel(TrailArgs a, P2PAr
     if (!ok_sh) return;
     TrailArgs b = a;
     b.rii = &rii_sh;
-    trail_body<RPT, CU, HP, CGS>(b, tile, group, wsum);
+    if (WIN)
+        trail_body_w<RPT, CU, CGS>(b, tile, group, wsum);
+    else
+        trail_body<RPT, CU, HP, CGS>(b, tile, group, wsum);
 }
 
 // Local R-row totals of step i (CTA c: column jbeg + c), sent to every rank;

@@ -117,3 +117,41 @@ def test_lockstep_one_rank_is_the_single_gpu_call():
         got = p2p.p2p_factorize_lockstep([Zd], ops, meth)[0]
         ref = aqr.factorize(Zd, aqr.CsrSpdOperator(ip, ix, dv), meth)
         assert torch.equal(got.Q, ref.Q) and torch.equal(got.R, ref.R), meth
+
+
+def test_multirank_big_tiles_windows_and_x_catchup():
+    """Local blocks of >= 2048 * 148 rows (the 2048-row tile path) and n = 20:
+    windowed trailing passes with write-backs and, for HP, the X catch-up,
+    across 2 emulated ranks (vs the oracle, R bitwise across ranks) and with
+    one rank (bitwise the single-GPU call)."""
+    import torch
+
+    import paper_1703_10440_b200 as aqr
+    from paper_1703_10440_b200 import distributed as DD
+    from paper_1703_10440_b200 import p2p, problems
+
+    g = 800  # 640,000 rows: 320,000 per rank
+    ip, ix, dv = problems.laplacian5(g, g, 1e-2)
+    Z = np.asfortranarray(problems.rng(23, 1).standard_normal((g * g, 20)))
+    m, n = Z.shape
+    spec = ("csr", ip, ix, dv)
+    meths = ("mgs-ha-row", "mgs-hp-row")
+    cal = parity.calibrated(Z, spec, meths)
+    part = DD.row_partition(m, 2, align=g)
+    ops = DD.DistCsrSpdOperator.blocks_of(ip, ix, dv, part)
+    blocks = [torch.from_numpy(np.ascontiguousarray(Z[r0:r1].T)).cuda().t() for r0, r1 in part]
+    seq = 1
+    for meth in meths:
+        res = p2p.p2p_factorize_lockstep(blocks, ops, meth, seq0=seq)
+        seq += n + 2
+        assert torch.equal(res[0].R, res[1].R), meth
+        Q = np.concatenate([r.Q.cpu().numpy() for r in res], axis=0)
+        o, tq, tr = cal[meth]
+        eq, er = parity.factor_errors(Q, res[0].R.cpu().numpy(), o.Q, o.R)
+        assert eq <= tq and er <= tr, (meth, eq, tq, er, tr)
+    Zd = torch.from_numpy(Z.T.copy()).cuda().t()
+    one = DD.DistCsrSpdOperator.blocks_of(ip, ix, dv, DD.row_partition(m, 1))
+    for meth in meths:
+        got = p2p.p2p_factorize_lockstep([Zd], one, meth)[0]
+        ref = aqr.factorize(Zd, aqr.CsrSpdOperator(ip, ix, dv), meth)
+        assert torch.equal(got.Q, ref.Q) and torch.equal(got.R, ref.R), meth
