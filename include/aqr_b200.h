@@ -164,7 +164,7 @@ AQR_API uint64_t aqr_pipe_workspace_bytes(int32_t family, int32_t variant, int32
 
 /* Column chunks the host-input pipeline uses for n columns (chunk_cols as
  * passed to aqr_gs_factor_pinned; 0 = the library's schedule; w > 0 uniform
- * chunks of w columns; -w doubling chunks w, w, 2w, 4w, ...): writes the
+ * chunks of w columns; -w a ramp w/8, w/4, w/2, then chunks of w): writes the
  * chunk boundaries (first 0, last n; at most max_bounds entries) and returns
  * the number of chunks.  A caller staging Z for the `ready` counter fills
  * chunk c = columns [bounds[c], bounds[c + 1]) in order. */

@@ -208,6 +208,10 @@ AQR_KNOB(dgemm_mode, "AQR_DGEMM", 1)
 // AQR_SPMM_SG=s: long-row SpMM (csr_spmm2_kernel) launch order, s column
 // blocks of 8 per super-group (0: all column blocks of a row block adjacent).
 AQR_KNOB(spmm_sg, "AQR_SPMM_SG", 4)
+// AQR_PIPE_MERGE=0: the host-input pipeline catches up one chunk at a time.
+AQR_KNOB(pipe_merge_mode, "AQR_PIPE_MERGE", 1)
+// AQR_XC_STREAM=0: the periodic X catch-up on the column-group grid too.
+AQR_KNOB(xc_stream_mode, "AQR_XC_STREAM", 1)
 // AQR_XC_ROWS=r: rows per thread of the X catch-up (1, 2 or 4; CTAs/SM 6 / 4 / 2;
 // config 5 HP catch-up 187 / 160 / 174 ms, profiles/r02/ab_xc_spmm.jsonl).
 AQR_KNOB(xc_rows_knob, "AQR_XC_ROWS", 2)
@@ -594,6 +598,15 @@ aqr_status launch_x_catchup(int64_t m, double *X, int64_t ldx, int64_t jbeg, int
     a.rstride = rstride;
     a.nk = (int32_t)nk;
     a.status = status;
+    if (nk <= aqr::kXsMaxK && xc_stream_mode() != 0) {  // one CTA per row block walks all columns
+        const long tix = timer_begin(3, (double)m * (16.0 * (double)(jend - jbeg) + 8.0 * (double)nk), s);
+        const size_t sm = aqr::xs_smem((int)nk);
+        AQR_TRY(ensure_smem(aqr::x_catchup_stream_kernel, sm));
+        const int64_t blocks = (m + aqr::kBlock * aqr::kXsRows - 1) / (aqr::kBlock * aqr::kXsRows);
+        launch_pdl(aqr::x_catchup_stream_kernel, dim3((unsigned)blocks), aqr::kBlock, sm, s, a);
+        timer_end(tix, s);
+        return launched("x_catchup_stream_kernel");
+    }
     const int64_t groups = (jend - jbeg + aqr::kXcCols - 1) / aqr::kXcCols;
     const int rpt = xc_rows();
     const int64_t rows = (m + aqr::kBlock * rpt - 1) / (aqr::kBlock * rpt);
@@ -995,8 +1008,22 @@ struct Run {
     // passes over it (totals by rrow_reduce into R).
     aqr_status make_live(int64_t i) {
         const size_t c = pp->next++;
-        const int64_t c0 = pp->bounds[c], c1 = pp->bounds[c + 1], w = c1 - c0;
-        AQR_CUDA(cudaStreamWaitEvent(s, pp->ev[c], 0));
+        const int64_t c0 = pp->bounds[c];
+        // Merge the chunks that have already arrived when the steps get here
+        // into one catch-up (i > 0): a wider chunk reloads the step vectors
+        // and the q window once per step for more columns.  The host waits
+        // for the compute stream to reach this point (one drain per chunk
+        // brought in), then takes every further chunk whose H2D is complete.
+        size_t c2 = c + 1;
+        if (i > 0 && pipe_merge_mode() != 0 && c2 < pp->ev.size()) {
+            AQR_CUDA(cudaStreamSynchronize(s));
+            while (c2 < pp->ev.size() && pp->bounds[c2 + 1] - c0 <= 512 && cudaEventQuery(pp->ev[c2]) == cudaSuccess)
+                ++c2;
+            (void)cudaGetLastError();  // (cudaErrorNotReady from the query is not an error)
+        }
+        pp->next = c2;
+        const int64_t c1 = pp->bounds[c2], w = c1 - c0;
+        for (size_t e = c; e < c2; ++e) AQR_CUDA(cudaStreamWaitEvent(s, pp->ev[e], 0));
         if (cgs)
             AQR_CUDA(copy_cols(col(Z0, m, c0), m, col(W, ldw, c0), ldw, m, w, cudaMemcpyDeviceToDevice, s));
         if (hp) {  // X = op.apply_block(Zw), chunk by chunk
@@ -1470,13 +1497,11 @@ int pipe_sched_mode() { return knob("AQR_PIPE_SCHED", 0); }  // read per call
 std::vector<int64_t> pipe_bounds(int64_t n, int64_t chunk_cols) {
     std::vector<int64_t> b{0};
     if (n <= 0) return b;
-    if (chunk_cols < 0) {  // doubling: w0, w0, 2 w0, 4 w0, ... (w0 = -chunk_cols)
-        int64_t c = 0, w = -chunk_cols;
-        b.push_back(c = std::min(n, w));
-        while (c < n) {
-            b.push_back(c = std::min(n, c + w));
-            w *= 2;
-        }
+    if (chunk_cols < 0) {  // ramp: w/8, w/4, w/2, then w (w = -chunk_cols)
+        const int64_t w = -chunk_cols;
+        int64_t c = 0;
+        for (int64_t r = std::max<int64_t>(1, w / 8); r < w && c < n; r *= 2) b.push_back(c = std::min(n, c + r));
+        while (c < n) b.push_back(c = std::min(n, c + w));
         return b;
     }
     const int sched = chunk_cols > 0 ? 0 : pipe_sched_mode();

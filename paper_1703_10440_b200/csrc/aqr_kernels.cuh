@@ -646,6 +646,68 @@ __global__ void __launch_bounds__(kBlock, MINB) x_catchup_kernel(XCatchArgs a) {
             if (ok[v] && c < nc) a.X[(int64_t)(j0 + c) * a.ldx + row0 + (int64_t)v * kBlock] = x[c][v];
 }
 
+// The periodic catch-up (nk <= kXsMaxK): one CTA per 512-row block walks
+// every column of [jbeg, jend) in groups of 8, with the block's p rows of
+// the window staged once in shared memory (thread-private rows, as the
+// trailing pass's q window) -- X read and written once, p read once, the
+// FP64 updates of a group overlapping the loads of the next.  Same rounding
+// sequence per element as x_catchup_kernel.
+constexpr int kXsRows = 2, kXsMaxK = 32;
+__host__ __device__ inline size_t xs_smem(int nk) { return sizeof(double) * (size_t)nk * kXsRows * kBlock; }
+__global__ void __launch_bounds__(kBlock, 3) x_catchup_stream_kernel(XCatchArgs a) {
+    extern __shared__ double xps[];  // [nk][kXsRows][kBlock]
+    __shared__ __align__(16) double rs[kXsMaxK][kXcCols];
+    pdl_wait();
+    if (failed(a.status)) return;
+    const int64_t row0 = (int64_t)blockIdx.x * (kBlock * kXsRows) + threadIdx.x;
+    bool ok[kXsRows];
+#pragma unroll
+    for (int v = 0; v < kXsRows; ++v) ok[v] = row0 + (int64_t)v * kBlock < a.m;
+    for (int k = 0; k < a.nk; ++k) {
+#pragma unroll
+        for (int v = 0; v < kXsRows; ++v)
+            xps[(k * kXsRows + v) * kBlock + threadIdx.x] =
+                ok[v] ? a.P[(int64_t)k * a.ldp + row0 + (int64_t)v * kBlock] : 0.0;
+    }
+    for (int j0 = a.jbeg; j0 < a.jend; j0 += kXcCols) {
+        const int nc = min(kXcCols, a.jend - j0);
+        double x[kXcCols][kXsRows];
+#pragma unroll
+        for (int c = 0; c < kXcCols; ++c)
+#pragma unroll
+            for (int v = 0; v < kXsRows; ++v)
+                x[c][v] = (ok[v] && c < nc) ? a.X[(int64_t)(j0 + c) * a.ldx + row0 + (int64_t)v * kBlock] : 0.0;
+        __syncthreads();  // the previous group's rs reads are done
+        for (int e = threadIdx.x; e < a.nk * kXcCols; e += kBlock) {
+            const int k = e / kXcCols, c = e - k * kXcCols;
+            rs[k][c] = c < nc ? __ldg(a.R + (int64_t)k * a.rstride + j0 + c) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int k = 0; k < a.nk; ++k) {
+            double pv[kXsRows], r[kXcCols];
+#pragma unroll
+            for (int v = 0; v < kXsRows; ++v) pv[v] = xps[(k * kXsRows + v) * kBlock + threadIdx.x];
+#pragma unroll
+            for (int c = 0; c < kXcCols; c += 2) {
+                const double2 rr = *reinterpret_cast<const double2 *>(&rs[k][c]);
+                r[c] = rr.x;
+                r[c + 1] = rr.y;
+            }
+#pragma unroll
+            for (int c = 0; c < kXcCols; ++c)
+#pragma unroll
+                for (int v = 0; v < kXsRows; ++v) x[c][v] = __dsub_rn(x[c][v], __dmul_rn(r[c], pv[v]));
+        }
+#pragma unroll
+        for (int c = 0; c < kXcCols; ++c)
+#pragma unroll
+            for (int v = 0; v < kXsRows; ++v)
+                if (ok[v] && c < nc) a.X[(int64_t)(j0 + c) * a.ldx + row0 + (int64_t)v * kBlock] = x[c][v];
+    }
+    pdl_trigger();
+}
+
 // Standalone totals of the norm partials (step API / multi-GPU driver).
 __global__ void __launch_bounds__(kBlock)
     norm_reduce_kernel(const double *npart, int32_t ntiles, double *tot, int64_t i, double *rii,

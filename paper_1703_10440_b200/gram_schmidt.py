@@ -189,12 +189,12 @@ def _gs_factor(Z, op, family, variant, orientation):
 
     host_in = not (D.is_torch(Z) and Z.is_cuda)
     if host_in:  # Z stays on the host; aqr_gs_factor_pinned streams it in
-        # 0: the library's schedule (n/8-column chunks).  HP: doubling chunks
-        # from n/16 (n/16, n/16, n/8, n/4, n/2): the first columns start the
-        # steps early, and the late chunks -- whose catch-ups replay most
-        # steps and reload the step vectors once per chunk and step -- are
-        # wide
-        chunk = _chunk_cols() or (-max(1, -(-n // 16)) if variant == "hp" else 0)
+        # 0: the library's schedule (n/8-column chunks).  HP: n/32-column
+        # chunks -- the steps start after the first few columns arrived, and
+        # the library merges the chunks already on the device into one
+        # catch-up (config 5 HP numpy end to end 1551 ms at n/16, 1532 ms at
+        # n/32; 1639 ms without merging)
+        chunk = _chunk_cols() or (max(1, -(-n // 32)) if variant == "hp" else 0)
         bounds = np.zeros(n + 1, dtype=np.int64)
         nch = int(L.aqr_pipe_chunks(n, chunk, bounds.ctypes.data, n + 1))
         staged = D.StagedHost(Z, bounds[: nch + 1])  # page-locked copy, filled while the device starts

@@ -82,6 +82,7 @@ def default_factors(tmp_path_factory):
     {"AQR_X_WIN": "3"},
     {"AQR_SPMM_SG": "0"},
     {"AQR_XC_ROWS": "4"},
+    {"AQR_XC_STREAM": "0"},
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},
     {"AQR_TRAIL_CTAS": "8"},

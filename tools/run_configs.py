@@ -4,7 +4,8 @@
 
 Prints one JSON line per (config, method): device time per factorization
 (CUDA events, after one warm-up), columns/s, the step-level algorithmic HBM
-bytes (SURVEY.md 8d model) and achieved GB/s, loss of A-orthogonality and
+bytes of this build's schedule (bench.step_bytes) and achieved GB/s, SURVEY
+8d's eager-model bytes for comparison, loss of A-orthogonality and
 ||Z - QR|| / ||Z||.  Config 5 (Z = 34 GB) and config 4 (A = 8.6 GB) are
 generated on the GPU (problems.config4 / config5).
 """
@@ -35,19 +36,17 @@ def timed(fn, reps=1):
     return e0.elapsed_time(e1) / reps, out
 
 
-def step_bytes(variant, m, n, bytes_A):
-    T = 8 * m * n * (n - 1)
-    mv = bytes_A + 16 * m
-    return {"ha": T + n * mv + 32 * m * n, "naive": T + 2 * n * mv + 32 * m * n,
-            "hp": 2 * T + (bytes_A + 16 * m * n) + 32 * m * n}[variant]
+from bench import step_bytes, survey_bytes  # noqa: E402  (this build's schedule model)
 
 
 def report(cfg, method, op, Z, bytes_A, reps=1, metrics=True):
     ms, r = timed(lambda: aqr.factorize(Z, op, method), reps)
     m, n = Z.shape
     b = step_bytes(method.split("-")[1], m, n, bytes_A)
+    e = survey_bytes(method.split("-")[1], m, n, bytes_A)
     line = {"config": cfg, "method": method, "m": m, "n": n, "ms": ms, "cols_per_s": n / (ms / 1e3),
-            "alg_GB": b / 1e9, "GBps": b / (ms / 1e3) / 1e9}
+            "alg_GB": b / 1e9, "GBps": b / (ms / 1e3) / 1e9, "survey_8d_GB": e / 1e9,
+            "survey_8d_equiv_GBps": e / (ms / 1e3) / 1e9}
     if metrics:
         line["loss_A_orth"] = aqr.loss_of_A_orthogonality(r.Q, op)
         line["residual_rel"] = aqr.residual_rel(Z, r.Q, r.R)
@@ -88,7 +87,8 @@ def main():
         torch.cuda.synchronize()
         print(json.dumps({"config": 5, "generated_s": time.time() - t0,
                           "mem_GB": torch.cuda.memory_allocated() / 1e9}), flush=True)
-        report(5, "mgs-hp-row", op, Z, 12 * op.nnz + 4 * (Z.shape[0] + 1), metrics=False)
+        for meth in ("mgs-hp-row", "mgs-ha-row"):
+            report(5, meth, op, Z, 12 * op.nnz + 4 * (Z.shape[0] + 1), metrics=False)
 
 
 if __name__ == "__main__":
