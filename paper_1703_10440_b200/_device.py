@@ -4,6 +4,8 @@ Column-major (Fortran) m x n device matrices are torch tensors of shape
 (m, n) with strides (1, ld): column j starts at data_ptr() + 8 * j * ld.
 """
 
+import os
+
 import numpy as np
 
 from ._lib import ExtensionUnavailable
@@ -89,7 +91,10 @@ def to_device_f(a, dev=None):
 # staging block comes from torch's page-locked cache, which keeps it alive
 # until the queued copies complete.
 _STAGE_MIN_BYTES = 64 << 20
-_STAGE_THREADS = 8
+# host threads copying pageable input into the page-locked staging block:
+# one per core (config 5, 34 GB: 8 threads are slower than the 55 GB/s PCIe
+# link; 16 threads stage at 91 GB/s, tools/stage_bench.py)
+_STAGE_THREADS = max(8, min(32, os.cpu_count() or 8))
 _pool = None
 
 

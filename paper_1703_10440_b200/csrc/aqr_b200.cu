@@ -208,6 +208,9 @@ AQR_KNOB(dgemm_mode, "AQR_DGEMM", 1)
 // AQR_SPMM_SG=s: long-row SpMM (csr_spmm2_kernel) launch order, s column
 // blocks of 8 per super-group (0: all column blocks of a row block adjacent).
 AQR_KNOB(spmm_sg, "AQR_SPMM_SG", 4)
+// AQR_SPLIT_LONG=0: HA steps with long CSR rows gather z and q_{j-1} in the
+// fused SpMV step instead of a separate update pass.
+AQR_KNOB(split_long_mode, "AQR_SPLIT_LONG", 1)
 // AQR_PIPE_MERGE=0: the host-input pipeline catches up one chunk at a time.
 AQR_KNOB(pipe_merge_mode, "AQR_PIPE_MERGE", 1)
 // AQR_XC_STREAM=0: the periodic X catch-up on the column-group grid too.
@@ -980,6 +983,8 @@ struct Run {
         return AQR_OK;
     }
 
+    bool long_rows() const { return a->op->max_row_nnz <= 0 || a->op->max_row_nnz > 8; }
+
     aqr::NormOut norm_out(int64_t j) const {
         aqr::NormOut o;
         o.npart = npart;
@@ -1122,6 +1127,19 @@ struct Run {
             AQR_TRY(launch_col_update_norm(m, z, qprev, x, pprev_col, r, nullptr, norm_out(j), true, s, pin, zs));
             zcol = (zs && !r) ? zs : z;  // without an update nothing was written to W
             xcol = x;
+        } else if (csr_native && r && long_rows() && split_long_mode() != 0) {
+            // long rows (> 8 entries, e.g. the 27-point stencil): the fused
+            // form would gather z AND q_{j-1} for every entry; instead the
+            // deferred update runs as one streaming pass (z_j -> zvec, with
+            // r_{j-1,j} and the rest of row j-1 of R from the partials) and
+            // the step kernel gathers the updated z only
+            double *xo = xout(j);
+            AQR_TRY(launch_col_update_norm(m, zvec, qprev, nullptr, nullptr, r, nullptr, no_norm(), false, s, pin,
+                                           zs ? zs : z));
+            AQR_TRY(launch_csr(a->op, 1, zvec, m, xo, m, nullptr, nullptr, nullptr, norm_out(j), s, nullptr));
+            ++mv;
+            zcol = zvec;
+            xcol = xo;
         } else if (csr_native) {
             // one fused launch: r_{j-1,j} (and the rest of row j-1 of R),
             // gather (z - r q), x = A z, z_new, norm, r_jj

@@ -13,7 +13,8 @@ without programmatic dependent launch, the materialized copy of Z, the
 column-oriented loop for the col methods (by default they run the
 row-oriented step schedule -- for HP that is also the eagerly updated X
 against the shipped lazy x), and the per-step catch-up launches of the
-host-input pipeline.
+host-input pipeline; the long-row (27-point) HA step with the deferred
+update fused into the SpMV gathers instead of a separate pass.
 """
 
 import os
@@ -43,6 +44,13 @@ for meth in ("mgs-ha-row", "mgs-hp-row", "cgs-ha-row", "cgs-hp-row", "mgs-naive-
     r = aqr.factorize(Zd, op, meth)
     out[meth + "|Q"] = r.Q.cpu().numpy()
     out[meth + "|R"] = r.R.cpu().numpy()
+s27 = problems.stencil27_device(70, 1e-2, "cuda")  # long rows (27-point), 343,000 rows
+op27 = aqr.CsrSpdOperator(*s27)
+Z27 = torch.from_numpy(problems.rng(9, 8).standard_normal((10, 70 ** 3))).cuda().t()
+for meth in ("mgs-ha-row", "cgs-ha-row", "mgs-hp-row"):
+    r = aqr.factorize(Z27, op27, meth)
+    out["st27|" + meth + "|Q"] = r.Q.cpu().numpy()
+    out["st27|" + meth + "|R"] = r.R.cpu().numpy()
 import os
 os.environ["AQR_CHUNK_COLS"] = "3"  # host input: the chunked pipeline and its catch-up
 Zn = np.asfortranarray(Z)
@@ -83,6 +91,7 @@ def default_factors(tmp_path_factory):
     {"AQR_SPMM_SG": "0"},
     {"AQR_XC_ROWS": "4"},
     {"AQR_XC_STREAM": "0"},
+    {"AQR_SPLIT_LONG": "0"},
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},
     {"AQR_TRAIL_CTAS": "8"},
