@@ -677,7 +677,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     a.trace = trace_slot();
     const int64_t ncols = std::max<int64_t>(0, (int64_t)a.jend - a.jbeg);
     if (a.ntiles == 0) return AQR_OK;
-    const bool big = aqr::rows_per_thread(a.m) == 8;
+    const bool big = aqr::rows_per_thread(a.m) == aqr::kBigRpt;
     // A persistent TMA-bulk (cp.async.bulk + mbarrier, warp-specialized)
     // form of this pass measured slower than this short-lived LDG kernel with
     // deferred totals (HA 9.26 vs 8.84 ms, HP 14.4 vs 14.1 ms on config 2;
@@ -700,7 +700,7 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     const long tix = timer_begin(0, trailing_bytes(a, hp, cgs, !hp), s);
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
     if (!hp) {
-        const int rpt = big ? 8 : 1;
+        const int rpt = big ? aqr::kBigRpt : 1;
         const size_t smw = aqr::trail_w_smem(rpt, std::max(a.cpg, 1), a.win);
 #define LAUNCHW(RPT, CU, CGS)                                                            \
     do {                                                                                 \
@@ -708,9 +708,9 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
         launch_pdl(aqr::trailing_w_kernel<RPT, CU, CGS>, grid, aqr::kBlock, smw, s, a); \
     } while (0)
 #ifdef AQR_EXPERIMENTS
-        if (big && !cgs && trail_cu() == 4) { LAUNCHW(8, 4, false); goto done; }
+        if (big && !cgs && trail_cu() == 4) { LAUNCHW(aqr::kBigRpt, 4, false); goto done; }
 #endif
-        if (big) { if (cgs) LAUNCHW(8, 2, true); else LAUNCHW(8, 2, false); }
+        if (big) { if (cgs) LAUNCHW(aqr::kBigRpt, 2, true); else LAUNCHW(aqr::kBigRpt, aqr::kBigCu, false); }
         else     { if (cgs) LAUNCHW(1, 4, true); else LAUNCHW(1, 4, false); }
 #undef LAUNCHW
         goto done;
@@ -727,9 +727,9 @@ aqr_status launch_trailing(const aqr::TrailArgs &a0, bool hp, bool cgs, cudaStre
     // 1 CTA/SM on config 2), CGS two (144 registers either way; 12 % faster).
     if (big) {
 #ifdef AQR_EXPERIMENTS
-        if (trail_variant() == 6 && !cgs) { LAUNCH(8, 2, true, false); goto done; }  // MGS-HP, two columns
+        if (trail_variant() == 6 && !cgs) { LAUNCH(aqr::kBigRpt, 2, true, false); goto done; }  // MGS-HP, two columns
 #endif
-        if (cgs) LAUNCH(8, 2, true, true); else LAUNCH(8, 1, true, false);
+        if (cgs) LAUNCH(aqr::kBigRpt, 2, true, true); else LAUNCH(aqr::kBigRpt, 1, true, false);
     } else {
         if (cgs) LAUNCH(1, 4, true, true); else LAUNCH(1, 4, true, false);
     }
@@ -884,7 +884,8 @@ aqr_status launch_catchup_t(const aqr::CatchArgs &c, cudaStream_t s) {
 }
 
 aqr_status launch_catchup(const aqr::CatchArgs &c, bool cgs, cudaStream_t s) {
-    if (aqr::rows_per_thread(c.m) == 8) return cgs ? launch_catchup_t<8, true>(c, s) : launch_catchup_t<8, false>(c, s);
+    if (aqr::rows_per_thread(c.m) == aqr::kBigRpt)
+        return cgs ? launch_catchup_t<aqr::kBigRpt, true>(c, s) : launch_catchup_t<aqr::kBigRpt, false>(c, s);
     return cgs ? launch_catchup_t<1, true>(c, s) : launch_catchup_t<1, false>(c, s);
 }
 
@@ -1275,13 +1276,14 @@ aqr_status launch_p2p_trailing(const aqr::TrailArgs &a0, const aqr::P2PArgs &P, 
     a.cpg = choose_cpg_generic(a.ntiles, ncols);
     a.ngroups = ncols > 0 ? (int32_t)((ncols + a.cpg - 1) / a.cpg) : 1;
     dim3 grid((unsigned)a.ntiles, (unsigned)a.ngroups);
-    const bool big = aqr::rows_per_thread(a.m) == 8;
-    const size_t smem = aqr::trail_w_smem(big ? 8 : 1, std::max(a.cpg, 1), a.win);
+    const bool big = aqr::rows_per_thread(a.m) == aqr::kBigRpt;
+    const size_t smem = aqr::trail_w_smem(big ? aqr::kBigRpt : 1, std::max(a.cpg, 1), a.win);
     if (a.win > 0) a.qprev = a.qwin + (int64_t)(a.win - 1) * a.ldw;  // trail_prefetch
     const long tix = timer_begin(0, trailing_bytes(a, false, CGS, true), s);
     if (big) {
-        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<8, 2, false, CGS, true>, smem));
-        launch_pdl(aqr::p2p_trailing_kernel<8, 2, false, CGS, true>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);
+        AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<aqr::kBigRpt, aqr::kBigCu, false, CGS, true>, smem));
+        launch_pdl(aqr::p2p_trailing_kernel<aqr::kBigRpt, aqr::kBigCu, false, CGS, true>, grid, aqr::kBlock, smem, s, a,
+                   P, i, rii, status);
     } else {
         AQR_TRY(ensure_smem(aqr::p2p_trailing_kernel<1, 4, false, CGS, true>, smem));
         launch_pdl(aqr::p2p_trailing_kernel<1, 4, false, CGS, true>, grid, aqr::kBlock, smem, s, a, P, i, rii, status);

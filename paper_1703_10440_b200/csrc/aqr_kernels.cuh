@@ -46,9 +46,15 @@ constexpr int kSpmmUnroll = AQR_SPMM_UNROLL;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 
-// Rows per thread of the reduction tile: depends on m only.
+// Rows per thread of the reduction tile: depends on m only (build-time
+// AQR_BIG_RPT for the large-m tile, 8 -> 2048-row tiles).
+#ifndef AQR_BIG_RPT
+#define AQR_BIG_RPT 8
+#endif
+constexpr int kBigRpt = AQR_BIG_RPT;
+constexpr int kBigCu = kBigRpt >= 8 ? 2 : 4;  // columns per iteration of the windowed pass at that tile
 __host__ __device__ inline int rows_per_thread(int64_t m) {
-    return m >= (int64_t)2048 * 148 ? 8 : 1;
+    return m >= (int64_t)2048 * 148 ? kBigRpt : 1;
 }
 __host__ __device__ inline int64_t tile_rows(int64_t m) { return (int64_t)kBlock * rows_per_thread(m); }
 __host__ __device__ inline int64_t num_tiles(int64_t m) {
@@ -923,7 +929,7 @@ __device__ __forceinline__ void trail_body(const TrailArgs &a, int tile, int gro
 // a prefetch never makes a later load stale.
 template <int RPT>
 __device__ __forceinline__ void trail_prefetch(const TrailArgs &a, int tile, int group) {
-    if (RPT != 8 || threadIdx.x != 0 || trail_prefetch_cols <= 0) return;
+    if (RPT < 4 || threadIdx.x != 0 || trail_prefetch_cols <= 0) return;
     const int64_t row0 = (int64_t)tile * (kBlock * RPT);
     const int64_t rows = min((int64_t)kBlock * RPT, a.m - row0);
     const uint32_t bytes = (uint32_t)(rows * 8) & ~15u;

@@ -46,7 +46,8 @@ def slots():
 res = {"device_ms": wall(lambda: aqr.factorize(Zd, op, meth))}
 Zp = torch.empty((n, m), dtype=torch.float64).pin_memory().t()
 Zp.copy_(Zd)
-Zh = np.asfortranarray(Zp.numpy())
+Zh = np.asfortranarray(Zp.numpy())  # numpy view of PAGE-LOCKED memory
+Zpg = np.asfortranarray(Zd.t().cpu().numpy().T)  # pageable numpy (the bench's e2e form)
 del Zd
 torch.cuda.empty_cache()
 for c in chunks:
@@ -58,5 +59,6 @@ for c in chunks:
     torch.cuda.synchronize()
     L.aqr_trailing_timer_enable(0)
     res[f"pinned_slots_chunk{c}"] = slots()
-    res[f"numpy_ms_chunk{c}"] = wall(lambda: aqr.factorize(Zh, op, meth))
+    res[f"numpy_pinned_src_ms_chunk{c}"] = wall(lambda: aqr.factorize(Zh, op, meth))
+    res[f"numpy_pageable_ms_chunk{c}"] = wall(lambda: aqr.factorize(Zpg, op, meth), 2)
 print(json.dumps(res))
