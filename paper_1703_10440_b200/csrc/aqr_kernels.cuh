@@ -991,6 +991,12 @@ __global__ void __launch_bounds__(kBlock, HP ? AQR_HP_MINB : 1) trailing_kernel(
 //
 // Shared memory (dynamic): wsum [kWarps][cpg], rsm [win][cpg] (r_kj of the
 // CTA's columns), qs [win][RPT][kBlock] (thread-private rows of q_k).
+// Column pairs ahead whose tiles the windowed pass bulk-prefetches into L2
+// (0: off; build-time knob).
+#ifndef AQR_TRAIL_PF_DIST
+#define AQR_TRAIL_PF_DIST 1  // config 5 HP trailing 931 / 900 / 909 / 955 ms at 0 / 1 / 2 / 4
+#endif
+constexpr int kTrailPfDist = AQR_TRAIL_PF_DIST;
 __host__ __device__ inline size_t trail_w_smem(int rpt, int cpg, int win) {
     return sizeof(double) * ((size_t)kWarps * cpg + (size_t)win * cpg + (size_t)win * rpt * kBlock);
 }
@@ -1047,7 +1053,20 @@ __device__ __forceinline__ void trail_body_w(const TrailArgs &a, int tile, int g
     const double *zb = a.Wsrc ? a.Wsrc : a.W;
     const int64_t ldzb = a.Wsrc ? a.ldwsrc : a.ldw;
 
+    // bytes of this tile in one column (16-byte multiple for the bulk prefetch)
+    const uint32_t pf_bytes = (uint32_t)(min((int64_t)kBlock * RPT, a.m - (int64_t)tile * kBlock * RPT) * 8) & ~15u;
     for (int j0 = cbeg; j0 < cend; j0 += CU) {
+        // keep HBM busy while the window arithmetic runs: the tile of the
+        // column pair kTrailPfDist pairs ahead is bulk-prefetched into L2
+        if (kTrailPfDist > 0 && RPT >= 4 && threadIdx.x == 0 && !CGS) {
+            const int jp = j0 + kTrailPfDist * CU;
+#pragma unroll
+            for (int c = 0; c < CU; ++c) {
+                const double *src = zb + (int64_t)(jp + c) * ldzb + (int64_t)tile * kBlock * RPT;
+                if (jp + c < cend && pf_bytes && ((uintptr_t)src & 15) == 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(pf_bytes) : "memory");
+            }
+        }
         // CGS reads z only where it is written (the dots use Z0)
         const bool needz = !CGS || (win > 0 && (a.store_all || j0 == a.jbeg));
         double z[CU][RPT], d0[CGS ? CU : 1][RPT];
@@ -1258,9 +1277,22 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
 #pragma unroll
                 for (int v = 0; v < RPT; ++v) qs[(kk * RPT + v) * kBlock + threadIdx.x] = qv[v];
             }
+            const uint32_t pf_bytes =
+                (uint32_t)(min((int64_t)kBlock * RPT, a.m - (int64_t)tile * kBlock * RPT) * 8) & ~15u;
             for (int g = g0; g < g1; ++g) {
                 const int c0 = g * CU;
                 const bool needz = !CGS || store;
+                // as the trailing pass: the next unit's tile toward L2 while this one computes
+                if (kTrailPfDist > 0 && RPT >= 4 && threadIdx.x == 0 && needz) {
+#pragma unroll
+                    for (int c = 0; c < CU; ++c) {
+                        const int cn = c0 + kTrailPfDist * CU + c;
+                        const double *src = a.W + (int64_t)(a.c0 + cn) * a.ldw + (int64_t)tile * kBlock * RPT;
+                        if (cn < g1 * CU && cn < a.w && pf_bytes && ((uintptr_t)src & 15) == 0)
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(pf_bytes)
+                                         : "memory");
+                    }
+                }
                 double z[CU][RPT], d0[CGS ? CU : 1][RPT], acc[CU];
 #pragma unroll
                 for (int c = 0; c < CU; ++c) {

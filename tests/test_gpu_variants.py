@@ -92,6 +92,7 @@ def default_factors(tmp_path_factory):
     {"AQR_XC_ROWS": "4"},
     {"AQR_XC_STREAM": "0"},
     {"AQR_SPLIT_LONG": "0"},
+    {"AQR_PIPE_MERGE": "0"},
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},
     {"AQR_TRAIL_CTAS": "8"},
