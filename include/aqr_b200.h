@@ -26,6 +26,9 @@
  *       by backend.kernels() (backend.py:66-68): seq_dot, sub_scaled,
  *       div_scalar, matvec, apply_block_dense, csr_matvec
  *       (_kernels_impl.py:17-56, 85-93)
+ *   aqr_block_apply                     <- SpdOperator.apply_block (58-66) as
+ *       the HP path calls it (gram_schmidt.py:136): dense operators on the
+ *       FP64 tensor cores, otherwise aqr_op_apply
  *   aqr_step_*                          <- the bodies of _gs_factor's
  *       project(i, j) (139-145) and normalize(j) (147-165), restated as the
  *       fused one-pass-per-step schedule used by the multi-GPU driver.

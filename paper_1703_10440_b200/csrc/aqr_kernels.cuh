@@ -675,8 +675,16 @@ __global__ void __launch_bounds__(kBlock, 3) x_catchup_stream_kernel(XCatchArgs 
             xps[(k * kXsRows + v) * kBlock + threadIdx.x] =
                 ok[v] ? a.P[(int64_t)k * a.ldp + row0 + (int64_t)v * kBlock] : 0.0;
     }
+    const int64_t rbase = (int64_t)blockIdx.x * (kBlock * kXsRows);
+    const uint32_t pf_bytes = (uint32_t)(min((int64_t)kBlock * kXsRows, a.m - rbase) * 8) & ~15u;
     for (int j0 = a.jbeg; j0 < a.jend; j0 += kXcCols) {
         const int nc = min(kXcCols, a.jend - j0);
+        if (threadIdx.x < kXcCols && pf_bytes) {  // the next group's block toward L2 (one column per thread)
+            const int jn = j0 + kXcCols + (int)threadIdx.x;
+            const double *src = a.X + (int64_t)jn * a.ldx + rbase;
+            if (jn < a.jend && ((uintptr_t)src & 15) == 0)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(pf_bytes) : "memory");
+        }
         double x[kXcCols][kXsRows];
 #pragma unroll
         for (int c = 0; c < kXcCols; ++c)
@@ -1184,6 +1192,9 @@ __host__ __device__ inline size_t catch_smem(int rpt, int w, int win, bool redun
                              (size_t)win * catch_wpad(w) + (size_t)win * rpt * kBlock);
 }
 
+#ifndef AQR_CATCHUP_PF
+#define AQR_CATCHUP_PF 1  // the catch-up's L2 look-ahead (build-time A/B)
+#endif
 #ifndef AQR_CATCHUP_REVERSE
 #define AQR_CATCHUP_REVERSE 1
 #endif
@@ -1283,7 +1294,7 @@ __global__ void __launch_bounds__(kBlock, 2) catchup_kernel(CatchArgs a) {
                 const int c0 = g * CU;
                 const bool needz = !CGS || store;
                 // as the trailing pass: the next unit's tile toward L2 while this one computes
-                if (kTrailPfDist > 0 && RPT >= 4 && threadIdx.x == 0 && needz) {
+                if (AQR_CATCHUP_PF && kTrailPfDist > 0 && RPT >= 4 && threadIdx.x == 0 && needz) {
 #pragma unroll
                     for (int c = 0; c < CU; ++c) {
                         const int cn = c0 + kTrailPfDist * CU + c;
