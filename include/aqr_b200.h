@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define AQR_ABI_VERSION 2
+#define AQR_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define AQR_API __attribute__((visibility("default")))
@@ -78,6 +78,22 @@ typedef enum {
 typedef int (*aqr_apply_fn)(void *ctx, int64_t k, const double *X, int64_t ldx, double *Y,
                             int64_t ldy, void *stream);
 
+/* Banded view of a CSR operator whose rows carry a fixed set of column
+ * offsets (stencils): built once by aqr_csr_band_create, attached to the
+ * operator through aqr_op.band.  The SpMV / SpMM kernels then form a row's
+ * gather addresses from its row number (4 bytes of mask per row instead of
+ * 12 bytes per entry); sums run in stored order, results are bitwise those
+ * of the CSR kernels (csr_matvec, _kernels_impl.py:50-56). */
+#define AQR_BAND_MAX 32
+typedef struct aqr_band {
+    int32_t nd;       /* distinct offsets col - row (0: the operator is not banded) */
+    int32_t constant; /* 1: every diagonal carries one value (val[d])             */
+    int64_t off[AQR_BAND_MAX]; /* ascending                                       */
+    double val[AQR_BAND_MAX];
+    const uint32_t *mask; /* device, m words: bit d = row has an entry at off[d]  */
+    const double *dvals;  /* device, nd x m diagonal-major values (constant == 0) */
+} aqr_band;
+
 typedef struct aqr_op {
     int32_t kind; /* aqr_op_kind */
     int32_t max_row_nnz; /* CSR: longest row (0 = unknown); picks the SpMV row batch, results unchanged */
@@ -97,7 +113,16 @@ typedef struct aqr_op {
     /* AQR_OP_DENSE: columns of A (0 = m, square).  A local row panel of a
      * row-partitioned operator is m_local x ncols (multi-GPU driver). */
     int64_t ncols;
+    /* AQR_OP_CSR: optional banded view (NULL: plain CSR kernels) */
+    const aqr_band *band;
 } aqr_op;
+
+/* Analyses a device CSR operator (ascending column indices per row, at most
+ * AQR_BAND_MAX distinct offsets, diagonals at least half populated) and
+ * allocates the view's device arrays; out->nd == 0 when the operator does
+ * not qualify (not an error).  Synchronizes `stream`. */
+AQR_API aqr_status aqr_csr_band_create(const aqr_op *csr, aqr_band *out, void *stream);
+AQR_API void aqr_csr_band_destroy(aqr_band *band);
 
 /* Everything _gs_factor takes and returns.  Inputs above the marker. */
 typedef struct aqr_factor_args {

@@ -13,7 +13,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # AQR_LIB_PATH: an alternative build of the same library (tools/ A/B experiments)
 LIB_PATH = os.environ.get("AQR_LIB_PATH") or os.path.join(_HERE, "libaqr_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 AQR_OK, AQR_EDIM, AQR_EBREAKDOWN, AQR_ECUDA, AQR_EARG, AQR_ENOMEM, AQR_ECALLBACK, AQR_ETIMEOUT = range(8)
 AQR_MGS, AQR_CGS = 0, 1
@@ -35,6 +35,17 @@ c_i32, c_i64, c_u64, c_dbl, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint
 APPLY_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp)
 
 
+BAND_MAX = 32
+
+
+class AqrBand(ctypes.Structure):
+    _fields_ = [
+        ("nd", c_i32), ("constant", c_i32),
+        ("off", c_i64 * BAND_MAX), ("val", c_dbl * BAND_MAX),
+        ("mask", c_vp), ("dvals", c_vp),
+    ]
+
+
 class AqrOp(ctypes.Structure):
     _fields_ = [
         ("kind", c_i32), ("max_row_nnz", c_i32), ("m", c_i64),
@@ -42,6 +53,7 @@ class AqrOp(ctypes.Structure):
         ("indptr", c_vp), ("indices", c_vp), ("data", c_vp), ("nnz", c_i64),
         ("apply", APPLY_FN), ("apply_block", APPLY_FN), ("ctx", c_vp),
         ("ncols", c_i64),
+        ("band", ctypes.POINTER(AqrBand)),
     ]
 
 
@@ -91,6 +103,8 @@ SIGNATURES = {
     "aqr_gs_factor_host": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_i32,
                                    c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.POINTER(c_i64),
                                    ctypes.POINTER(c_dbl), c_vp, ctypes.POINTER(c_i64)]),
+    "aqr_csr_band_create": (c_i32, [ctypes.POINTER(AqrOp), ctypes.POINTER(AqrBand), c_vp]),
+    "aqr_csr_band_destroy": (None, [ctypes.POINTER(AqrBand)]),
     "aqr_op_apply": (c_i32, [ctypes.POINTER(AqrOp), c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_block_apply": (c_i32, [ctypes.POINTER(AqrOp), c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "aqr_dot": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),

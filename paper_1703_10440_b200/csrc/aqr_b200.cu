@@ -29,6 +29,7 @@
 #include "aqr_dense.cuh"
 #include "aqr_dgemm.cuh"
 #include "aqr_kernels.cuh"
+#include "aqr_band.cuh"
 #include "aqr_p2p.cuh"
 
 namespace {
@@ -211,6 +212,8 @@ AQR_KNOB(spmm_sg, "AQR_SPMM_SG", 4)
 // AQR_SPLIT_LONG=0: HA steps with long CSR rows gather z and q_{j-1} in the
 // fused SpMV step instead of a separate update pass.
 AQR_KNOB(split_long_mode, "AQR_SPLIT_LONG", 1)
+// AQR_BAND=0: ignore an operator's banded view (plain CSR kernels).
+AQR_KNOB(band_mode, "AQR_BAND", 1)
 // AQR_PIPE_MERGE=0: the host-input pipeline catches up one chunk at a time.
 AQR_KNOB(pipe_merge_mode, "AQR_PIPE_MERGE", 1)
 // AQR_XC_STREAM=0: the periodic X catch-up on the column-group grid too.
@@ -284,6 +287,50 @@ aqr::NormOut no_norm() {
     return o;
 }
 
+// ---- banded view of a CSR operator (aqr_band.cuh) ------------------------------
+// Offsets per row rounded up to an instantiated width; a mask bit is never
+// set for d >= nd, so the wider kernel computes the same sums.
+template <int ND, bool CONST>
+void launch_band_nd(const aqr::BandArgs &b, bool step, unsigned grid, cudaStream_t s) {
+    if (step) {  // fused HA / naive step or plain y = A x on the canonical norm grid
+        constexpr int U = ND <= 8 ? 2 : 1;
+        launch_pdl(aqr::band_step_kernel<ND, CONST, U, AQR_SPMV_MINB>, grid, aqr::kBlock, 0, s, b);
+    } else {
+        aqr::band_spmm_kernel<ND, CONST, 8, 4, 2><<<grid, aqr::kBlock, 0, s>>>(b);
+    }
+}
+
+template <bool CONST>
+void launch_band_c(const aqr::BandArgs &b, bool step, unsigned grid, cudaStream_t s) {
+    const int nd = b.b.nd;
+    if (nd <= 5) launch_band_nd<5, CONST>(b, step, grid, s);
+    else if (nd <= 7) launch_band_nd<7, CONST>(b, step, grid, s);
+    else if (nd <= 9) launch_band_nd<9, CONST>(b, step, grid, s);
+    else if (nd <= 16) launch_band_nd<16, CONST>(b, step, grid, s);
+    else if (nd <= 27) launch_band_nd<27, CONST>(b, step, grid, s);
+    else launch_band_nd<32, CONST>(b, step, grid, s);
+}
+
+void launch_band(const aqr::CsrArgs &a, const aqr_band *band, bool step, unsigned grid, cudaStream_t s) {
+    aqr::BandArgs b;
+    b.c = a;
+    b.b.nd = band->nd;
+    b.b.constant = band->constant;
+    for (int d = 0; d < aqr::kBandMax; ++d) {
+        b.b.off[d] = d < band->nd ? band->off[d] : 0;
+        b.b.val[d] = d < band->nd ? band->val[d] : 0.0;
+    }
+    b.b.mask = band->mask;
+    b.b.dvals = band->dvals;
+    if (band->constant) launch_band_c<true>(b, step, grid, s);
+    else launch_band_c<false>(b, step, grid, s);
+}
+
+bool band_usable(const aqr_op *op) {
+    return op->band != nullptr && op->band->nd > 0 && op->band->nd <= aqr::kBandMax && op->band->mask != nullptr &&
+           (op->band->constant || op->band->dvals != nullptr) && band_mode() != 0;
+}
+
 aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx, double *Y,
                       int64_t ldy, const double *qprev, const double *r, double *znew,
                       const aqr::NormOut &out, cudaStream_t s, const aqr::RrowIn *rin = nullptr) {
@@ -319,7 +366,9 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         // known and <= 8 (all of a row's loads in one batch, no predicated-off
         // slots); longer rows loop.  AQR_SPMV_VARIANT=3: unpipelined, B = 8.
         const int32_t mr = op->max_row_nnz;
-        if (sv == 3)
+        if (band_usable(op))
+            launch_band(a, op->band, true, g1, s);
+        else if (sv == 3)
             launch_pdl(aqr::csr_step_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
         else if (mr >= 1 && mr <= 4)
             launch_pdl(aqr::csr_step_pf_kernel<4, AQR_SPMV_MINB>, g1, aqr::kBlock, 0, s, a);
@@ -338,6 +387,15 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
     }
     const int32_t mr = op->max_row_nnz;
     const int plain_pf = plain_pf_mode();
+    if (band_usable(op) && k == 1) {  // plain y = A x on the banded view
+        launch_band(a, op->band, true, (unsigned)aqr::norm_tiles(op->m, false), s);
+        return launched("band_step_kernel");
+    }
+    if (band_usable(op) && k > 1 && (mr > 8 || mr <= 0)) {  // long rows: CTA = (8 columns, 256 rows)
+        const int64_t nb = (op->m + aqr::kBlock - 1) / aqr::kBlock;
+        launch_band(a, op->band, false, (unsigned)(((k + 7) / 8) * nb), s);
+        return launched("band_spmm_kernel");
+    }
     if (k == 1 && mr >= 1 && mr <= 8 && plain_pf != 0 && AQR_SPMV_PF2 != 0) {
         // plain y = A x through the pipelined step kernel (no norms, no
         // update): rows three deep instead of one dependent chain per row
@@ -2071,6 +2129,10 @@ aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientati
     }
     if (st == AQR_OK && cudaMemcpyAsync(Q, Z_host, 8 * (size_t)m * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
         st = set_err(AQR_ECUDA, "H2D Z");
+    aqr_band band;  // stencil operators run on the banded view (nd == 0: plain CSR)
+    std::memset(&band, 0, sizeof band);
+    if (st == AQR_OK && op_kind == AQR_OP_CSR && aqr_csr_band_create(&op, &band, s) == AQR_OK && band.nd > 0)
+        op.band = &band;
     aqr_factor_args a;
     std::memset(&a, 0, sizeof a);
     if (st == AQR_OK) {
@@ -2094,6 +2156,7 @@ aqr_status aqr_gs_factor_host(int32_t family, int32_t variant, int32_t orientati
         if (fail_val) *fail_val = a.fail_val;
         if (mv_count) *mv_count = a.mv_count;
     }
+    aqr_csr_band_destroy(&band);
     cleanup();
     return st;
 }
@@ -2167,6 +2230,79 @@ aqr_status aqr_csr_matvec(int64_t m, const int32_t *indptr, const int32_t *indic
     op.indices = indices;
     op.data = data;
     return aqr_op_apply(&op, 1, x, m, y, m, stream);
+}
+
+// ---- banded view of a CSR operator (aqr_band.cuh) -----------------------------
+
+aqr_status aqr_csr_band_create(const aqr_op *csr, aqr_band *out, void *stream) {
+    if (!out) return set_err(AQR_EARG, "null band");
+    std::memset(out, 0, sizeof *out);
+    if (!csr || csr->kind != AQR_OP_CSR || !csr->indptr || (csr->nnz && (!csr->indices || !csr->data)))
+        return set_err(AQR_EARG, "band analysis needs a CSR operator");
+    const int64_t m = csr->m, nnz = csr->nnz;
+    if (m < 1 || nnz < 1) return AQR_OK;
+    cudaStream_t s = S(stream);
+    aqr::BandScan *sc = nullptr;
+    uint32_t *mask = nullptr;
+    double *dvals = nullptr;
+    auto fail = [&](aqr_status st, const char *msg) {
+        cudaFree(sc);
+        cudaFree(mask);
+        cudaFree(dvals);
+        return msg ? set_err(st, msg) : st;
+    };
+    if (cudaMalloc(&sc, sizeof(aqr::BandScan)) != cudaSuccess) return fail(AQR_ENOMEM, "band: device allocation failed");
+    const unsigned grid = (unsigned)((m + aqr::kBlock - 1) / aqr::kBlock);
+    aqr::band_scan_init_kernel<<<1, 64, 0, s>>>(sc);
+    aqr::band_collect_kernel<<<grid, aqr::kBlock, 0, s>>>(m, csr->indptr, csr->indices, sc);
+    aqr::BandScan h;
+    if (cudaMemcpyAsync(&h, sc, sizeof h, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(AQR_ECUDA, "band: offset scan failed");
+    std::vector<int64_t> offs;
+    for (int i = 0; i < aqr::kBandSlots; ++i)
+        if (h.keys[i] != aqr::kBandEmpty) offs.push_back((int64_t)h.keys[i]);
+    // not banded: too many offsets, unsorted rows, or diagonals less than half populated
+    if (h.bad || offs.empty() || offs.size() > (size_t)aqr::kBandMax || 2 * nnz < (int64_t)offs.size() * m)
+        return fail(AQR_OK, nullptr);
+    std::sort(offs.begin(), offs.end());
+    aqr::BandDesc d;
+    std::memset(&d, 0, sizeof d);
+    d.nd = (int32_t)offs.size();
+    for (int i = 0; i < d.nd; ++i) d.off[i] = offs[(size_t)i];
+    if (cudaMalloc(&mask, 4 * (size_t)m) != cudaSuccess) return fail(AQR_ENOMEM, "band: device allocation failed");
+    aqr::band_mask_kernel<<<grid, aqr::kBlock, 0, s>>>(m, csr->indptr, csr->indices, csr->data, d, mask, sc);
+    if (cudaMemcpyAsync(&h, sc, sizeof h, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(AQR_ECUDA, "band: mask pass failed");
+    if (h.bad) return fail(AQR_OK, nullptr);
+    if (h.varying) {
+        if (cudaMalloc(&dvals, 8 * (size_t)m * (size_t)d.nd) != cudaSuccess)
+            return fail(AQR_OK, nullptr);  // no room for the diagonal-major values: stay on CSR
+        cudaMemsetAsync(dvals, 0, 8 * (size_t)m * (size_t)d.nd, s);
+        aqr::band_vals_kernel<<<grid, aqr::kBlock, 0, s>>>(m, csr->indptr, csr->indices, csr->data, d, dvals);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return fail(AQR_ECUDA, "band: value pass failed");
+    }
+    cudaFree(sc);
+    out->nd = d.nd;
+    out->constant = h.varying ? 0 : 1;
+    for (int i = 0; i < d.nd; ++i) {
+        out->off[i] = d.off[i];
+        const long long bits = (long long)h.first[i];
+        double v;
+        std::memcpy(&v, &bits, 8);
+        out->val[i] = h.varying ? 0.0 : v;
+    }
+    out->mask = mask;
+    out->dvals = dvals;
+    return AQR_OK;
+}
+
+void aqr_csr_band_destroy(aqr_band *band) {
+    if (!band) return;
+    cudaFree(const_cast<uint32_t *>(band->mask));
+    cudaFree(const_cast<double *>(band->dvals));
+    std::memset(band, 0, sizeof *band);
 }
 
 // ---- dense helpers in the reference's order (aqr_dense.cuh) -----------------

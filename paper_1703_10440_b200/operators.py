@@ -181,7 +181,9 @@ class CsrSpdOperator(SpdOperator):
     kernel's row batch (results are identical for every value).
     """
 
-    def __init__(self, indptr, indices, data, dim=None, max_row_nnz=None):
+    def __init__(self, indptr, indices, data, dim=None, max_row_nnz=None, banded=None):
+        self._band = None
+        self.banded = banded  # None: use the banded view when the operator qualifies; False: never
         if D.is_torch(indptr):
             self._init_device(indptr, indices, data, dim)
         else:
@@ -250,8 +252,31 @@ class CsrSpdOperator(SpdOperator):
             d.m = self.dim
             d.indptr, d.indices, d.data = ip.data_ptr(), ix.data_ptr(), dv.data_ptr()
             d.nnz = self.nnz
+            if self.banded is None or self.banded:
+                # stencil operators: offsets + row masks instead of per-entry
+                # indices (aqr_csr_band_create; nd == 0 when it does not qualify)
+                band = _lib.AqrBand()
+                _lib.check(_lib.lib().aqr_csr_band_create(ctypes.byref(d), ctypes.byref(band), D.stream_ptr()),
+                           "aqr_csr_band_create")
+                if band.nd > 0:
+                    self._band = band
+                    d.band = ctypes.pointer(band)
             self._desc = d
         return self._desc
+
+    @property
+    def band_offsets(self):
+        """Column offsets of the banded view (None when the CSR kernels run)."""
+        self._native()
+        return None if self._band is None else [int(self._band.off[i]) for i in range(self._band.nd)]
+
+    def __del__(self):
+        band, self._band = getattr(self, "_band", None), None
+        if band is not None and band.nd > 0:
+            try:
+                _lib.lib().aqr_csr_band_destroy(ctypes.byref(band))
+            except Exception:  # interpreter shutdown
+                pass
 
     def to_dense(self):
         indptr = np.asarray(self.indptr.cpu() if D.is_torch(self.indptr) else self.indptr)

@@ -154,7 +154,10 @@ def test_pipeline_chunk_schedule(n):
 
 def test_ctypes_struct_layout_matches_header():
     # aqr_op / aqr_factor_args as declared in include/aqr_b200.h (LP64)
-    assert ctypes.sizeof(_lib.AqrOp) == 4 + 4 + 8 + 8 + 8 + 8 * 3 + 8 + 8 * 3 + 8
+    assert ctypes.sizeof(_lib.AqrOp) == 4 + 4 + 8 + 8 + 8 + 8 * 3 + 8 + 8 * 3 + 8 + 8
+    assert _lib.AqrOp.band.offset == ctypes.sizeof(_lib.AqrOp) - 8
+    # aqr_band: nd, constant, off[32], val[32], mask, dvals
+    assert ctypes.sizeof(_lib.AqrBand) == 4 + 4 + 8 * 32 + 8 * 32 + 8 + 8
     assert _lib.AqrFactorArgs.flagged_host.offset == 4 * 4 + 8 * 2 + 8 * 6 + 8 + 8 + 8 + 8 + 8 + 8
     # aqr_p2p_group: 2 x int32, 3 arrays of AQR_MAX_RANKS (8) pointers / int64, n_halo, 2 pointers,
     # seq0, timeout_ns

@@ -1,7 +1,9 @@
 """A/B of schedule knobs: per-slot kernel times of one factorization.
 
     AQR_LIB_PATH=paper_1703_10440_b200/libaqr_b200_exp.so AQR_TRAIL_WIN=4 \
-        python tools/kernel_ab.py [method] [config 2|5] [reps]
+        python tools/kernel_ab.py [method] [config 2|3|5] [reps]
+
+AQR_BANDED=0 builds the operator without the banded view (plain CSR kernels).
 
 Prints one JSON line: the step time (CUDA events, K factorizations back to
 back) and, from a second pass with the library's kernel timer on, per slot
@@ -17,13 +19,14 @@ L = _lib.lib()
 meth = sys.argv[1] if len(sys.argv) > 1 else "mgs-ha-row"
 cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 K = int(sys.argv[3]) if len(sys.argv) > 3 else (5 if cfg == 2 else 2)
+banded = None if os.environ.get("AQR_BANDED", "1") != "0" else False  # 0: plain CSR kernels
 if cfg == 5:
     csr, Zd = problems.config5()
-    op = aqr.CsrSpdOperator(*csr)
+    op = aqr.CsrSpdOperator(*csr, banded=banded)
     del csr
 else:
-    (ip, ix, dv), Z = problems.config2(device=False)
-    op = aqr.CsrSpdOperator(ip, ix, dv)
+    (ip, ix, dv), Z = problems.config3(device=False) if cfg == 3 else problems.config2(device=False)
+    op = aqr.CsrSpdOperator(ip, ix, dv, banded=banded)
     Zd = torch.from_numpy(Z.T).cuda().t()
 for _ in range(2 if cfg == 5 else 3):
     r = aqr.factorize(Zd, op, meth)
@@ -42,7 +45,7 @@ for _ in range(K):
     del r
 torch.cuda.synchronize()
 knobs = {k: v for k, v in os.environ.items() if k.startswith("AQR_")}
-out = {"knobs": knobs, "method": meth, "config": cfg, "step_ms": step}
+out = {"knobs": knobs, "method": meth, "config": cfg, "band": op.band_offsets is not None, "step_ms": step}
 for slot, name in ((0, "trailing"), (1, "spmv_step"), (2, "col_update"), (3, "x_catchup"), (4, "block_apply")):
     n, ms, b = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
     L.aqr_kernel_timer_read(slot, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(b))
