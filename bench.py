@@ -402,6 +402,13 @@ def run_b200(args, rank, world, local_rank):
     m, n = wl["m"], wl["n"]
     bytes_A, nnz = bytes_of_A(wl)
     op = aqr.DenseSpdOperator(wl["dense"]) if "dense" in wl else aqr.CsrSpdOperator(*wl["csr"])
+    op_layout = "dense" if "dense" in wl else "csr"
+    if "csr" in wl and op.band_offsets is not None:
+        # stencil operator on the banded view (csrc/aqr_band.cuh): a 4-byte row mask
+        # (+ the values diagonal-major when the diagonals are not constant) per apply
+        nd = len(op.band_offsets)
+        bytes_A = 4 * m + (0 if op._band.constant else 8 * nd * m)
+        op_layout = f"banded view of the CSR operator ({nd} offsets, {'constant' if op._band.constant else 'varying'} diagonals)"
     wl.pop("csr", None)
     wl.pop("dense", None)
     Zd = wl["Z"]
@@ -461,7 +468,8 @@ def run_b200(args, rank, world, local_rank):
     }
     sb = step_bytes(variant, m, n, bytes_A)
     step_gbs = sb / (ms_per_step / 1e3) / 1e9
-    roofline["step"] = {"achieved": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": sb}
+    roofline["step"] = {"achieved": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes": sb,
+                        "operator_layout": op_layout, "operator_bytes_per_apply": bytes_A}
     # what SURVEY 8d's eager one-pass schedule would have to move in the same time
     eager = survey_bytes(variant, m, n, bytes_A)
     roofline["step"]["survey_8d_bytes"] = eager

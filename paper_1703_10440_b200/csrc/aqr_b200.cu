@@ -214,6 +214,9 @@ AQR_KNOB(spmm_sg, "AQR_SPMM_SG", 4)
 AQR_KNOB(split_long_mode, "AQR_SPLIT_LONG", 1)
 // AQR_BAND=0: ignore an operator's banded view (plain CSR kernels).
 AQR_KNOB(band_mode, "AQR_BAND", 1)
+// AQR_BAND_STAGE=0: the block apply of long banded rows gathers from global
+// memory instead of staging the operand segments in shared memory.
+AQR_KNOB(band_stage_mode, "AQR_BAND_STAGE", 1)
 // AQR_PIPE_MERGE=0: the host-input pipeline catches up one chunk at a time.
 AQR_KNOB(pipe_merge_mode, "AQR_PIPE_MERGE", 1)
 // AQR_XC_STREAM=0: the periodic X catch-up on the column-group grid too.
@@ -290,28 +293,92 @@ aqr::NormOut no_norm() {
 // ---- banded view of a CSR operator (aqr_band.cuh) ------------------------------
 // Offsets per row rounded up to an instantiated width; a mask bit is never
 // set for d >= nd, so the wider kernel computes the same sums.
+#ifndef AQR_BAND_RPT
+#define AQR_BAND_RPT 4  // staged SpMM: 256-row sub-blocks per CTA
+#endif
+#ifndef AQR_BAND_KC
+#define AQR_BAND_KC 8   // staged SpMM: columns per CTA
+#endif
+#ifndef AQR_BAND_SPMM_MINB
+#define AQR_BAND_SPMM_MINB 2
+#endif
+
+// Segments of the operand a block of NB rows reads (offsets closer than NB
+// apart share one); false when they do not fit the staged kernels.
+bool band_stage_plan(const aqr_band *band, int64_t NB, aqr::BandStage *st) {
+    std::memset(st, 0, sizeof *st);
+    int ns = -1;
+    int64_t hi = 0, total = 0;
+    for (int d = 0; d < band->nd; ++d) {
+        const int64_t off = band->off[d];
+        if (ns < 0 || off > hi + 32) {  // a new segment (small gaps are staged through)
+            if (ns >= 0) {
+                st->len[ns] = (int32_t)(hi - st->lo[ns]);
+                total += (st->len[ns] + 1) & ~1;
+            }
+            if (++ns >= aqr::kBandSegMax) return false;
+            st->lo[ns] = off;
+            st->base[ns] = (int32_t)total;
+        }
+        hi = off + NB;
+        if (total + (off - st->lo[ns]) + NB > (int64_t)1 << 20) return false;
+        st->sbyte[d] = 8 * (st->base[ns] + (int32_t)(off - st->lo[ns]));
+    }
+    if (ns < 0) return false;
+    st->len[ns] = (int32_t)(hi - st->lo[ns]);
+    total += (st->len[ns] + 1) & ~1;
+    st->nseg = ns + 1;
+    st->total = (int32_t)total;
+    return 2 * total * 8 <= 200 * 1024;  // two buffers
+}
+
 template <int ND, bool CONST>
-void launch_band_nd(const aqr::BandArgs &b, bool step, unsigned grid, cudaStream_t s) {
+aqr_status launch_band_tile(const aqr::BandArgs &b, const aqr_band *band, cudaStream_t s) {
+    aqr::BandTileArgs t;
+    t.c = b.c;
+    t.b = b.b;
+    constexpr int NB = AQR_BAND_RPT * aqr::kBlock;
+    if (!band_stage_plan(band, NB, &t.st)) return AQR_EARG;
+    auto kern = aqr::band_spmm_tile_kernel<ND, CONST, AQR_BAND_RPT, AQR_BAND_KC, AQR_BAND_SPMM_MINB>;
+    const size_t smem = 2 * (size_t)t.st.total * 8;
+    AQR_TRY(ensure_smem(kern, smem));
+    const int64_t grid = ((b.c.m + NB - 1) / NB) * ((b.c.k + AQR_BAND_KC - 1) / AQR_BAND_KC);
+    kern<<<(unsigned)grid, aqr::kBlock, smem, s>>>(t);
+    return AQR_OK;
+}
+
+template <int ND, bool CONST>
+void launch_band_nd(const aqr::BandArgs &b, bool step, cudaStream_t s) {
+    const int64_t m = b.c.m;
     if (step) {  // fused HA / naive step or plain y = A x on the canonical norm grid
-        constexpr int U = ND <= 8 ? 2 : 1;
-        launch_pdl(aqr::band_step_kernel<ND, CONST, U, AQR_SPMV_MINB>, grid, aqr::kBlock, 0, s, b);
-    } else {
-        aqr::band_spmm_kernel<ND, CONST, 8, 4, 2><<<grid, aqr::kBlock, 0, s>>>(b);
+        constexpr int U = ND <= 5 ? AQR_BAND_U5 : (ND <= 9 ? AQR_BAND_U9 : 1);
+        launch_pdl(aqr::band_step_kernel<ND, CONST, U, AQR_SPMV_MINB>, (unsigned)aqr::norm_tiles(m, false),
+                   aqr::kBlock, 0, s, b);
+    } else {  // CTA = (8 columns, 256 rows)
+        const int64_t nb = (m + aqr::kBlock - 1) / aqr::kBlock;
+        aqr::band_spmm_kernel<ND, CONST, 8, 4, 2><<<(unsigned)(((b.c.k + 7) / 8) * nb), aqr::kBlock, 0, s>>>(b);
     }
 }
 
 template <bool CONST>
-void launch_band_c(const aqr::BandArgs &b, bool step, unsigned grid, cudaStream_t s) {
+void launch_band_c(const aqr::BandArgs &b, const aqr_band *band, bool step, cudaStream_t s) {
     const int nd = b.b.nd;
-    if (nd <= 5) launch_band_nd<5, CONST>(b, step, grid, s);
-    else if (nd <= 7) launch_band_nd<7, CONST>(b, step, grid, s);
-    else if (nd <= 9) launch_band_nd<9, CONST>(b, step, grid, s);
-    else if (nd <= 16) launch_band_nd<16, CONST>(b, step, grid, s);
-    else if (nd <= 27) launch_band_nd<27, CONST>(b, step, grid, s);
-    else launch_band_nd<32, CONST>(b, step, grid, s);
+    if (!step && nd > 9 && band_stage_mode() != 0) {  // long rows, k > 1: operands staged in shared memory
+        aqr_status st = AQR_EARG;
+        if (nd <= 16) st = launch_band_tile<16, CONST>(b, band, s);
+        else if (nd <= 27) st = launch_band_tile<27, CONST>(b, band, s);
+        else st = launch_band_tile<32, CONST>(b, band, s);
+        if (st == AQR_OK) return;
+    }
+    if (nd <= 5) launch_band_nd<5, CONST>(b, step, s);
+    else if (nd <= 7) launch_band_nd<7, CONST>(b, step, s);
+    else if (nd <= 9) launch_band_nd<9, CONST>(b, step, s);
+    else if (nd <= 16) launch_band_nd<16, CONST>(b, step, s);
+    else if (nd <= 27) launch_band_nd<27, CONST>(b, step, s);
+    else launch_band_nd<32, CONST>(b, step, s);
 }
 
-void launch_band(const aqr::CsrArgs &a, const aqr_band *band, bool step, unsigned grid, cudaStream_t s) {
+void launch_band(const aqr::CsrArgs &a, const aqr_band *band, bool step, cudaStream_t s) {
     aqr::BandArgs b;
     b.c = a;
     b.b.nd = band->nd;
@@ -322,8 +389,8 @@ void launch_band(const aqr::CsrArgs &a, const aqr_band *band, bool step, unsigne
     }
     b.b.mask = band->mask;
     b.b.dvals = band->dvals;
-    if (band->constant) launch_band_c<true>(b, step, grid, s);
-    else launch_band_c<false>(b, step, grid, s);
+    if (band->constant) launch_band_c<true>(b, band, step, s);
+    else launch_band_c<false>(b, band, step, s);
 }
 
 bool band_usable(const aqr_op *op) {
@@ -367,7 +434,7 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         // slots); longer rows loop.  AQR_SPMV_VARIANT=3: unpipelined, B = 8.
         const int32_t mr = op->max_row_nnz;
         if (band_usable(op))
-            launch_band(a, op->band, true, g1, s);
+            launch_band(a, op->band, true, s);
         else if (sv == 3)
             launch_pdl(aqr::csr_step_kernel<8, 3>, g1, aqr::kBlock, 0, s, a);
         else if (mr >= 1 && mr <= 4)
@@ -388,12 +455,11 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
     const int32_t mr = op->max_row_nnz;
     const int plain_pf = plain_pf_mode();
     if (band_usable(op) && k == 1) {  // plain y = A x on the banded view
-        launch_band(a, op->band, true, (unsigned)aqr::norm_tiles(op->m, false), s);
+        launch_band(a, op->band, true, s);
         return launched("band_step_kernel");
     }
     if (band_usable(op) && k > 1 && (mr > 8 || mr <= 0)) {  // long rows: CTA = (8 columns, 256 rows)
-        const int64_t nb = (op->m + aqr::kBlock - 1) / aqr::kBlock;
-        launch_band(a, op->band, false, (unsigned)(((k + 7) / 8) * nb), s);
+        launch_band(a, op->band, false, s);
         return launched("band_spmm_kernel");
     }
     if (k == 1 && mr >= 1 && mr <= 8 && plain_pf != 0 && AQR_SPMV_PF2 != 0) {

@@ -19,6 +19,18 @@ namespace aqr {
 
 constexpr int kBandMax = 32;  // == AQR_BAND_MAX (include/aqr_b200.h)
 
+// Build knobs (A/B): diagonals per batch of gathers in the step kernel, and
+// owned rows per iteration for <= 5 / 6-9 offsets (longer rows: 1).
+#ifndef AQR_BAND_DB
+#define AQR_BAND_DB 9
+#endif
+#ifndef AQR_BAND_U5
+#define AQR_BAND_U5 2
+#endif
+#ifndef AQR_BAND_U9
+#define AQR_BAND_U9 1
+#endif
+
 struct BandDesc {
     int32_t nd;
     int32_t constant;
@@ -139,17 +151,20 @@ __global__ void __launch_bounds__(kBlock) band_vals_kernel(int64_t m, const int3
 // b, b+G, ..., one row per thread, the norm chains in ascending block order.
 // U owned rows per iteration: their mask loads, then all gathers (addresses
 // from the row number), then the sums in offset order.
-template <int ND, bool CONST, int U>
+// FULL: every row of the warp carries all ND offsets (interior rows of the
+// grid): no predicates.
+template <int ND, bool CONST, int U, bool FULL, bool UPD>
 __device__ __forceinline__ void band_step_rows(const BandArgs &A, const int64_t (&row)[U], const uint32_t (&mk)[U],
-                                               bool upd, double rj, double &t, double &zz, double &xx) {
+                                               double rj, double &t, double &zz, double &xx) {
+    constexpr bool upd = UPD;
     const CsrArgs &a = A.c;
-    constexpr int DB = ND <= 9 ? ND : 9;  // diagonals per batch of gathers
+    constexpr int DB = ND <= AQR_BAND_DB ? ND : AQR_BAND_DB;  // diagonals per batch of gathers
     double y[U], zc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         y[u] = 0.0;
-        zc[u] = row[u] < a.m ? a.X[row[u]] : 0.0;
-        if (upd) zc[u] = __dsub_rn(zc[u], __dmul_rn(rj, row[u] < a.m ? a.qprev[row[u]] : 0.0));
+        zc[u] = (FULL || row[u] < a.m) ? a.X[row[u]] : 0.0;
+        if (upd) zc[u] = __dsub_rn(zc[u], __dmul_rn(rj, (FULL || row[u] < a.m) ? a.qprev[row[u]] : 0.0));
     }
 #pragma unroll
     for (int d0 = 0; d0 < ND; d0 += DB) {
@@ -157,16 +172,19 @@ __device__ __forceinline__ void band_step_rows(const BandArgs &A, const int64_t 
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int h = 0; h < DB; ++h)
-                xv[u][h] = (d0 + h < ND && (mk[u] >> (d0 + h) & 1u)) ? __ldg(a.X + row[u] + A.b.off[(d0 + h) % ND]) : 0.0;
+            for (int h = 0; h < DB; ++h) {
+                const bool has = d0 + h < ND && (FULL || (mk[u] >> (d0 + h) & 1u));
+                xv[u][h] = has ? __ldg(a.X + row[u] + A.b.off[(d0 + h) % ND]) : 0.0;
+            }
         if (upd) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 double qv[DB];
 #pragma unroll
-                for (int h = 0; h < DB; ++h)
-                    qv[h] = (d0 + h < ND && (mk[u] >> (d0 + h) & 1u)) ? __ldg(a.qprev + row[u] + A.b.off[(d0 + h) % ND])
-                                                                      : 0.0;
+                for (int h = 0; h < DB; ++h) {
+                    const bool has = d0 + h < ND && (FULL || (mk[u] >> (d0 + h) & 1u));
+                    qv[h] = has ? __ldg(a.qprev + row[u] + A.b.off[(d0 + h) % ND]) : 0.0;
+                }
 #pragma unroll
                 for (int h = 0; h < DB; ++h) xv[u][h] = __dsub_rn(xv[u][h], __dmul_rn(rj, qv[h]));
             }
@@ -175,7 +193,7 @@ __device__ __forceinline__ void band_step_rows(const BandArgs &A, const int64_t 
         for (int u = 0; u < U; ++u)
 #pragma unroll
             for (int h = 0; h < DB; ++h)
-                if (d0 + h < ND && (mk[u] >> (d0 + h) & 1u)) {
+                if (d0 + h < ND && (FULL || (mk[u] >> (d0 + h) & 1u))) {
                     const int d = (d0 + h) % ND;
                     const double v = CONST ? A.b.val[d] : __ldg(A.b.dvals + (int64_t)d * a.m + row[u]);
                     y[u] = __dadd_rn(y[u], __dmul_rn(v, xv[u][h]));
@@ -183,7 +201,7 @@ __device__ __forceinline__ void band_step_rows(const BandArgs &A, const int64_t 
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        if (row[u] >= a.m) continue;
+        if (!FULL && row[u] >= a.m) continue;
         a.Y[row[u]] = y[u];
         if (a.znew) a.znew[row[u]] = zc[u];
         t = fma(zc[u], y[u], t);
@@ -211,6 +229,7 @@ __global__ void __launch_bounds__(kBlock, MINB) band_step_kernel(BandArgs A) {
     const bool upd = a.r != nullptr;
     const double rj = a.rin.partial ? rrow_first(a.rin, cta == 0) : (upd ? *a.r : 0.0);
     const int64_t nblk = (a.m + kBlock - 1) / kBlock;
+    const uint32_t full = A.b.nd >= 32 ? 0xffffffffu : (1u << A.b.nd) - 1u;
     double t = 0.0, zz = 0.0, xx = 0.0;
     for (int64_t blk = cta; blk < nblk; blk += (int64_t)U * G) {
         int64_t nrow[U];
@@ -220,7 +239,19 @@ __global__ void __launch_bounds__(kBlock, MINB) band_step_kernel(BandArgs A) {
             nrow[u] = row[u] + U * stride;
             nmk[u] = nrow[u] < a.m ? __ldg(A.b.mask + nrow[u]) : 0u;
         }
-        band_step_rows<ND, CONST, U>(A, row, mk, upd, rj, t, zz, xx);
+        // interior warps of short stencils skip the predicates (config 2 fused
+        // step 21.0 -> 19.2 us, config 3 65 -> 57 us); with 27 offsets the two
+        // unrolled paths spill and the step is slower (98 -> 117 ms on config 5)
+        bool fullw = ND <= 9 && A.b.nd == ND;
+#pragma unroll
+        for (int u = 0; u < U; ++u) fullw &= mk[u] == full;
+        if (ND <= 9 && __all_sync(0xffffffffu, fullw)) {
+            if (upd) band_step_rows<ND, CONST, U, true, true>(A, row, mk, rj, t, zz, xx);
+            else band_step_rows<ND, CONST, U, true, false>(A, row, mk, rj, t, zz, xx);
+        } else {
+            if (upd) band_step_rows<ND, CONST, U, false, true>(A, row, mk, rj, t, zz, xx);
+            else band_step_rows<ND, CONST, U, false, false>(A, row, mk, rj, t, zz, xx);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) row[u] = nrow[u], mk[u] = nmk[u];
     }
@@ -282,6 +313,145 @@ __global__ void __launch_bounds__(kBlock, MINB) band_spmm_kernel(BandArgs A) {
 #pragma unroll
     for (int kk = 0; kk < K; ++kk)
         if (col0 + kk < a.k) a.Y[row + (col0 + kk) * a.ldy] = acc[kk];
+}
+
+// ---- staged tiles: Y = A X with long rows (27-point stencils) ----------------------
+// With many offsets per row the gather kernel above is bound by instruction
+// issue and the L1 data path (27 8-byte gathers per row and column).  A
+// block of NB consecutive rows needs, per offset d, the NB consecutive
+// elements x[r0 + off_d ..]; offsets closer than NB apart overlap, so the
+// union is a few contiguous segments (a 27-point stencil on an n^3 grid
+// with NB >= n: three, one per grid plane).  The CTA copies the segments of
+// a column into shared memory with asynchronous copies (cp.async, no
+// registers), double-buffered so the next column's copies run under the
+// current column's arithmetic, and every row reads its operands from there
+// (one shared-memory load per operand, its address a per-offset constant
+// plus the thread's base).  Same operands, same order, same rounding as the
+// gather kernels.
+constexpr int kBandSegMax = 8;
+
+struct BandStage {
+    int32_t nseg;
+    int32_t total;                // doubles of shared memory per buffer
+    int64_t lo[kBandSegMax];      // first offset of the segment (relative to r0)
+    int32_t len[kBandSegMax];     // elements staged
+    int32_t base[kBandSegMax];    // shared-memory index of the segment
+    int32_t sbyte[kBandMax];      // shared-memory byte offset of (row r0, offset d)
+};
+
+struct BandTileArgs {
+    CsrArgs c;
+    BandDesc b;
+    BandStage st;
+};
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Issues the copies of one column's segments for the row block at r0.
+// Elements outside [0, m) are skipped: no row reads them (its mask bit for
+// that offset is clear).
+__device__ __forceinline__ void band_stage_async(const BandStage &st, const double *__restrict__ x, int64_t r0,
+                                                 int64_t m, double *sm, bool inside) {
+    for (int s = 0; s < st.nseg; ++s) {
+        const int64_t g0 = r0 + st.lo[s];
+        const double *src = x + g0;
+        double *dst = sm + st.base[s];
+        const int len = st.len[s];
+        if (inside) {
+#pragma unroll 4
+            for (int e = threadIdx.x; e < len; e += kBlock) cp_async8(dst + e, src + e);
+        } else {
+            for (int e = threadIdx.x; e < len; e += kBlock)
+                if (g0 + e >= 0 && g0 + e < m) cp_async8(dst + e, src + e);
+        }
+    }
+}
+
+// CTA = (block of RPT x 256 rows, KC columns), thread = rows tid + 256 i of
+// the block.  Launch order as csr_spmm2_kernel (super-groups of a.sg column
+// groups).
+template <int ND, bool CONST, int RPT, int KC, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) band_spmm_tile_kernel(BandTileArgs A) {
+    extern __shared__ double band_sm[];  // two buffers of st.total doubles
+    const CsrArgs &a = A.c;
+    constexpr int NB = RPT * kBlock;
+    const int64_t ncb = (a.k + KC - 1) / KC;
+    const int64_t nrb = (a.m + NB - 1) / NB;
+    const int64_t sg = (a.sg > 0 && a.sg < ncb) ? a.sg : ncb;
+    const int64_t per_sg = sg * nrb;
+    const int64_t g = blockIdx.x / per_sg, rest = blockIdx.x - g * per_sg;
+    const int64_t w = min(sg, ncb - g * sg);
+    const int64_t rb = rest / w, cb = g * sg + rest % w;
+    const int64_t r0 = rb * NB;
+    uint32_t mk[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int64_t row = r0 + threadIdx.x + i * kBlock;
+        mk[i] = row < a.m ? __ldg(A.b.mask + row) : 0u;
+    }
+    const uint32_t full = A.b.nd >= 32 ? 0xffffffffu : (1u << A.b.nd) - 1u;
+    bool interior = A.b.nd == ND;  // the unpredicated path runs all ND offsets
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) interior &= mk[i] == full;
+    interior = __all_sync(0xffffffffu, interior);  // one path per warp
+    const int last = A.st.nseg - 1;
+    const bool inside = r0 + A.st.lo[0] >= 0 && r0 + A.st.lo[last] + A.st.len[last] <= a.m;
+    const int64_t cend = min(a.k, (cb + 1) * KC);
+    int64_t col = cb * KC;
+    band_stage_async(A.st, a.X + col * a.ldx, r0, a.m, band_sm, inside);
+    cp_async_commit();
+    for (int c = 0; col < cend; ++col, ++c) {
+        double *buf = band_sm + (c & 1) * A.st.total;
+        if (col + 1 < cend)
+            band_stage_async(A.st, a.X + (col + 1) * a.ldx, r0, a.m, band_sm + ((c & 1) ^ 1) * A.st.total, inside);
+        cp_async_commit();
+        cp_async_wait<1>();  // this column's copies (all groups but the newest) have landed
+        __syncthreads();
+        const char *sp0 = reinterpret_cast<const char *>(buf + threadIdx.x);
+        double y[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) y[i] = 0.0;
+        if (interior) {  // all of this thread's rows carry every offset: no predicates
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                const double *sp = reinterpret_cast<const double *>(sp0 + A.st.sbyte[d]);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const double v = CONST ? A.b.val[d]
+                                           : __ldg(A.b.dvals + (int64_t)d * a.m + r0 + threadIdx.x + i * kBlock);
+                    y[i] = __dadd_rn(y[i], __dmul_rn(v, sp[i * kBlock]));
+                }
+            }
+        } else {  // branch-free: the sum is formed and kept only where the entry exists
+#pragma unroll
+            for (int d = 0; d < ND; ++d) {
+                const double *sp = reinterpret_cast<const double *>(sp0 + A.st.sbyte[d]);
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const bool has = mk[i] >> d & 1u;
+                    const double v = CONST ? A.b.val[d]
+                                           : (has ? __ldg(A.b.dvals + (int64_t)d * a.m + r0 + threadIdx.x + i * kBlock)
+                                                  : 0.0);
+                    const double yn = __dadd_rn(y[i], __dmul_rn(v, sp[i * kBlock]));
+                    y[i] = has ? yn : y[i];
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int64_t row = r0 + threadIdx.x + i * kBlock;
+            if (row < a.m) a.Y[row + col * a.ldy] = y[i];
+        }
+        __syncthreads();  // the buffer is free for the column after next
+    }
 }
 
 }  // namespace aqr

@@ -47,6 +47,9 @@ CASES = {
     "diff7": (lambda: _diff7(11), [-121, -11, -1, 0, 1, 11, 121], False),
     "st27": (lambda: _st27(9), sorted((dz * 9 + dy) * 9 + dx for dz in (-1, 0, 1) for dy in (-1, 0, 1)
                                       for dx in (-1, 0, 1)), True),
+    # three staged segments (the grid planes are further apart than a row block)
+    "st27b": (lambda: _st27(21), sorted((dz * 21 + dy) * 21 + dx for dz in (-1, 0, 1) for dy in (-1, 0, 1)
+                                        for dx in (-1, 0, 1)), True),
 }
 
 
@@ -130,7 +133,7 @@ def test_factorization_bitwise(aqr, name, method):
     assert list(rb.flagged_columns) == list(rp.flagged_columns)
 
 
-@pytest.mark.parametrize("name", ["lap5", "st27"])
+@pytest.mark.parametrize("name", ["lap5", "st27", "st27b"])
 def test_vs_oracle(aqr, name):
     import parity
 

@@ -14,7 +14,9 @@ column-oriented loop for the col methods (by default they run the
 row-oriented step schedule -- for HP that is also the eagerly updated X
 against the shipped lazy x), and the per-step catch-up launches of the
 host-input pipeline; the long-row (27-point) HA step with the deferred
-update fused into the SpMV gathers instead of a separate pass.
+update fused into the SpMV gathers instead of a separate pass; the plain CSR
+kernels instead of the banded view of the stencil operators, and the banded
+view's gather kernels instead of its shared-memory staged tiles.
 """
 
 import os
@@ -92,6 +94,9 @@ def default_factors(tmp_path_factory):
     {"AQR_XC_ROWS": "4"},
     {"AQR_XC_STREAM": "0"},
     {"AQR_SPLIT_LONG": "0"},
+    {"AQR_BAND": "0"},
+    {"AQR_BAND_STAGE": "0"},
+    {"AQR_BAND": "0", "AQR_SPLIT_LONG": "0"},
     {"AQR_PIPE_MERGE": "0"},
     {"AQR_TRAIL_VARIANT": "6"},
     {"AQR_LDG_REVERSE": "0"},

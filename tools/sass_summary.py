@@ -4,13 +4,14 @@
 
 For every kernel: instruction count and the opcodes that show which
 hardware path it uses -- UTMALDG / UBLKCP (TMA tensor / bulk copies),
+LDGSTS (cp.async copies into shared memory),
 SYNCS (mbarriers), DMMA (FP64 tensor cores), DFMA / DMUL / DADD (FP64
 pipe), LDG / STG / LDS, and the demangled kernel name."""
 import collections, re, subprocess, sys
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_1703_10440_b200/libaqr_b200.so"
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
-KEYS = ["UTMALDG", "UBLKCP", "UBLKPF", "SYNCS", "DMMA", "DFMA", "DMUL", "DADD", "LDG", "STG", "LDS", "STS",
+KEYS = ["UTMALDG", "UBLKCP", "UBLKPF", "LDGSTS", "SYNCS", "DMMA", "DFMA", "DMUL", "DADD", "LDG", "STG", "LDS", "STS",
         "ATOMG", "RED", "SHFL", "BAR"]
 funcs, cur = collections.OrderedDict(), None
 for line in sass.splitlines():
