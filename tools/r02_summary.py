@@ -33,7 +33,9 @@ def launches(path):
 
 def short(name):
     for key in ("trailing_w_kernel", "trailing_kernel", "col_lazy_norm_kernel", "x_catchup_kernel",
-                "csr_spmm2_kernel", "finalize_r_kernel", "status_init_kernel", "dense_dmma_kernel"):
+                "csr_spmm2_kernel", "finalize_r_kernel", "status_init_kernel", "dense_dmma_kernel",
+                "band_spmm_tile_kernel", "band_spmm_kernel", "band_step_kernel", "band_collect_kernel",
+                "band_mask_kernel", "band_vals_kernel"):
         if key in name:
             return key
     return name.split("(")[0][-50:]
