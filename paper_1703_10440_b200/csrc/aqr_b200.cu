@@ -363,7 +363,10 @@ void launch_band_nd(const aqr::BandArgs &b, bool step, cudaStream_t s) {
 template <bool CONST>
 void launch_band_c(const aqr::BandArgs &b, const aqr_band *band, bool step, cudaStream_t s) {
     const int nd = b.b.nd;
-    if (!step && nd > 9 && band_stage_mode() != 0) {  // long rows, k > 1: operands staged in shared memory
+    // long rows, k > 1: operands staged in shared memory.  (The k = 1 step staged the
+    // same way -- cp.async, double-buffered over the CTA's owned row blocks -- measured
+    // 104 vs 100 ms per config-5 HA factorization and is not kept.)
+    if (!step && nd > 9 && band_stage_mode() != 0) {
         aqr_status st = AQR_EARG;
         if (nd <= 16) st = launch_band_tile<16, CONST>(b, band, s);
         else if (nd <= 27) st = launch_band_tile<27, CONST>(b, band, s);
