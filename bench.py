@@ -255,6 +255,18 @@ def device_workload(cfg, rank=0, world=1):
     return {"csr": csr, "Z": Z, "m": Z.shape[0], "n": Z.shape[1]}
 
 
+def banded_bytes(op, m):
+    """(bytes per apply, description) of a CsrSpdOperator on the banded view
+    (csrc/aqr_band.cuh): a 4-byte row mask, plus the values diagonal-major when
+    the diagonals are not constant; None when the CSR kernels run."""
+    offs = getattr(op, "band_offsets", None)
+    if offs is None:
+        return None
+    nd, const = len(offs), bool(op._band.constant)
+    return (4 * m + (0 if const else 8 * nd * m),
+            f"banded view of the CSR operator ({nd} offsets, {'constant' if const else 'varying'} diagonals)")
+
+
 def bytes_of_A(wl):
     if "dense" in wl:
         return 8 * wl["m"] * wl["m"], None
@@ -403,12 +415,8 @@ def run_b200(args, rank, world, local_rank):
     bytes_A, nnz = bytes_of_A(wl)
     op = aqr.DenseSpdOperator(wl["dense"]) if "dense" in wl else aqr.CsrSpdOperator(*wl["csr"])
     op_layout = "dense" if "dense" in wl else "csr"
-    if "csr" in wl and op.band_offsets is not None:
-        # stencil operator on the banded view (csrc/aqr_band.cuh): a 4-byte row mask
-        # (+ the values diagonal-major when the diagonals are not constant) per apply
-        nd = len(op.band_offsets)
-        bytes_A = 4 * m + (0 if op._band.constant else 8 * nd * m)
-        op_layout = f"banded view of the CSR operator ({nd} offsets, {'constant' if op._band.constant else 'varying'} diagonals)"
+    if "csr" in wl and banded_bytes(op, m) is not None:
+        bytes_A, op_layout = banded_bytes(op, m)
     wl.pop("csr", None)
     wl.pop("dense", None)
     Zd = wl["Z"]

@@ -354,7 +354,7 @@ void launch_band_nd(const aqr::BandArgs &b, bool step, cudaStream_t s) {
         constexpr int U = ND <= 5 ? AQR_BAND_U5 : (ND <= 9 ? AQR_BAND_U9 : 1);
         launch_pdl(aqr::band_step_kernel<ND, CONST, U, AQR_SPMV_MINB>, (unsigned)aqr::norm_tiles(m, false),
                    aqr::kBlock, 0, s, b);
-    } else {  // CTA = (8 columns, 256 rows)
+    } else if constexpr (ND >= 9) {  // CTA = (8 columns, 256 rows); rows of <= 8 entries run csr_row_kernel
         const int64_t nb = (m + aqr::kBlock - 1) / aqr::kBlock;
         aqr::band_spmm_kernel<ND, CONST, 8, 4, 2><<<(unsigned)(((b.c.k + 7) / 8) * nb), aqr::kBlock, 0, s>>>(b);
     }

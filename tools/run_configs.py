@@ -36,15 +36,17 @@ def timed(fn, reps=1):
     return e0.elapsed_time(e1) / reps, out
 
 
-from bench import step_bytes, survey_bytes  # noqa: E402  (this build's schedule model)
+from bench import banded_bytes, step_bytes, survey_bytes  # noqa: E402  (this build's schedule model)
 
 
 def report(cfg, method, op, Z, bytes_A, reps=1, metrics=True):
     ms, r = timed(lambda: aqr.factorize(Z, op, method), reps)
     m, n = Z.shape
-    b = step_bytes(method.split("-")[1], m, n, bytes_A)
+    bb = banded_bytes(op, m)  # stencil operators: the banded view's bytes per apply
+    b = step_bytes(method.split("-")[1], m, n, bb[0] if bb else bytes_A)
     e = survey_bytes(method.split("-")[1], m, n, bytes_A)
-    line = {"config": cfg, "method": method, "m": m, "n": n, "ms": ms, "cols_per_s": n / (ms / 1e3),
+    line = {"config": cfg, "method": method, "m": m, "n": n, "operator": bb[1] if bb else "as given",
+            "ms": ms, "cols_per_s": n / (ms / 1e3),
             "alg_GB": b / 1e9, "GBps": b / (ms / 1e3) / 1e9, "survey_8d_GB": e / 1e9,
             "survey_8d_equiv_GBps": e / (ms / 1e3) / 1e9}
     if metrics:
