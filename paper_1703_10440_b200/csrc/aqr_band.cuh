@@ -30,6 +30,9 @@ constexpr int kBandMax = 32;  // == AQR_BAND_MAX (include/aqr_b200.h)
 #ifndef AQR_BAND_U9
 #define AQR_BAND_U9 1
 #endif
+#ifndef AQR_BAND_PF
+#define AQR_BAND_PF 1  // 1 / 2: prefetch the next row's operands into L1 / L2 (6-9 offsets); 0: off
+#endif
 
 struct BandDesc {
     int32_t nd;
@@ -39,6 +42,14 @@ struct BandDesc {
     const uint32_t *mask;   // [m]
     const double *dvals;    // [nd][m] when !constant
 };
+
+__device__ __forceinline__ void band_prefetch(const double *p) {
+#if AQR_BAND_PF == 1
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#endif
+}
 
 struct BandArgs {
     CsrArgs c;  // indptr / indices / data unused
@@ -239,6 +250,26 @@ __global__ void __launch_bounds__(kBlock, MINB) band_step_kernel(BandArgs A) {
             nrow[u] = row[u] + U * stride;
             nmk[u] = nrow[u] < a.m ? __ldg(A.b.mask + nrow[u]) : 0u;
         }
+#if AQR_BAND_PF
+        // one row per iteration (6-9 offsets): the next owned row's operands on
+        // their way into the cache while this row's gathers are in flight (rows
+        // whose whole offset range lies inside the vector; the others just
+        // miss).  Config 3 fused step 57 -> 53 us (L1 and L2 alike); with two
+        // rows per iteration (<= 5 offsets) it costs: config 2 19.2 -> 21.2 us.
+        if (U == 1 && ND <= 9) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (nrow[u] + A.b.off[0] >= 0 && nrow[u] + A.b.off[(ND - 1) % kBandMax] < a.m &&
+                    A.b.off[(ND - 1) % kBandMax] != 0) {
+#pragma unroll
+                    for (int d = 0; d < ND; ++d) {
+                        band_prefetch(a.X + nrow[u] + A.b.off[d]);
+                        if (upd) band_prefetch(a.qprev + nrow[u] + A.b.off[d]);
+                        if (!CONST) band_prefetch(A.b.dvals + (int64_t)d * a.m + nrow[u]);
+                    }
+                }
+        }
+#endif
         // interior warps of short stencils skip the predicates (config 2 fused
         // step 21.0 -> 19.2 us, config 3 65 -> 57 us); with 27 offsets the two
         // unrolled paths spill and the step is slower (98 -> 117 ms on config 5)
