@@ -461,7 +461,8 @@ aqr_status launch_csr(const aqr_op *op, int64_t k, const double *X, int64_t ldx,
         launch_band(a, op->band, true, s);
         return launched("band_step_kernel");
     }
-    if (band_usable(op) && k > 1 && (mr > 8 || mr <= 0)) {  // long rows: CTA = (8 columns, 256 rows)
+    // long rows (>= 9 offsets; narrower views have no k > 1 kernel and run the CSR ones)
+    if (band_usable(op) && k > 1 && (mr > 8 || mr <= 0) && op->band->nd >= 9) {
         launch_band(a, op->band, false, s);
         return launched("band_spmm_kernel");
     }

@@ -116,6 +116,11 @@ def test_products_bitwise(aqr, name):
     for k in (2, 8, 13):
         X = np.asfortranarray(rng.standard_normal((m, k)))
         assert np.array_equal(band.apply_block(X), plain.apply_block(X))
+    # an unknown row length (hint 0) takes the long-row route whatever the view's width
+    hint0 = aqr.CsrSpdOperator(*csr, max_row_nnz=0)
+    X = np.asfortranarray(rng.standard_normal((m, 5)))
+    assert np.array_equal(hint0.apply_block(X), plain.apply_block(X))
+    assert np.array_equal(hint0.apply(x), yp)
 
 
 @pytest.mark.parametrize("name", list(CASES))
