@@ -91,11 +91,32 @@ def to_device_f(a, dev=None):
 # staging block comes from torch's page-locked cache, which keeps it alive
 # until the queued copies complete.
 _STAGE_MIN_BYTES = 64 << 20
-# host threads copying pageable input into the page-locked staging block:
-# one per core (config 5, 34 GB: 8 threads are slower than the 55 GB/s PCIe
-# link; 16 threads stage at 91 GB/s, tools/stage_bench.py)
-_STAGE_THREADS = max(8, min(32, os.cpu_count() or 8))
-_pool = None
+# host threads copying pageable input into the page-locked staging block.
+# Alone, 16 threads stage at 83-91 GB/s (tools/stage_bench.py), but inside the
+# factorization call the copies compete with the H2D / D2H DMA for host
+# memory bandwidth.  Wide problems are compute-bound (device time ~ n x the
+# transfer time / 170): there the staging only has to keep loosely ahead, and
+# with 16 threads the first chunks reach the device every 43 ms instead of
+# every 20 ms (tools/pipe_trace.py mgs-hp-row 5 numpy) -- the device idles
+# through the first half second.  Config 5 HP (n = 256), numpy in / numpy out
+# on a 16-core host (tools/e2e_repeat.py, AQR_STAGE_THREADS sweep): 1.70-1.78 s
+# with 16 threads, 1.65-1.71 (8), 1.58-1.67 (6), 1.55-1.64 (4), 1.63 (3),
+# 1.83 (2).  Narrow problems are transfer-bound and want the full staging
+# rate: config 2 / 3 HA (n = 64 / 128) 21.5 / 85.9 ms with 8 threads,
+# 22.9 / 86.0 (16), 25.1-25.7 / 104 (4).  AQR_STAGE_THREADS overrides both.
+_STAGE_THREADS = int(os.environ.get("AQR_STAGE_THREADS", "0"))
+_pools = {}
+
+
+def _stage_pool(n_cols=0):
+    """The host staging pool for an input of ``n_cols`` columns."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cores = os.cpu_count() or 4
+    size = _STAGE_THREADS or (max(2, min(4, cores)) if n_cols >= 192 else max(2, min(8, cores)))
+    if size not in _pools:
+        _pools[size] = ThreadPoolExecutor(size, thread_name_prefix="aqr-h2d")
+    return _pools[size]
 
 
 class StagedHost:
@@ -118,12 +139,8 @@ class StagedHost:
         if is_torch(a) and a.is_pinned() and a.dtype == t.float64 and leading_dim(a) is not None:
             self.T, self.ld, self.ready, self._futs = a, leading_dim(a), None, []
             return
-        global _pool
-        if _pool is None:
-            from concurrent.futures import ThreadPoolExecutor
-
-            _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="aqr-h2d")
         m, n = a.shape
+        _pool = _stage_pool(n)
         self.stage = t.empty((n, m), dtype=t.float64, pin_memory=True)
         self.T, self.ld = self.stage.t(), max(m, 1)
         self.flag = t.zeros(1, dtype=t.int32, pin_memory=True)
@@ -166,17 +183,13 @@ class StagedHost:
 
 
 def _h2d_staged(A, dev):
-    global _pool
     t = torch()
     m, n = A.shape
-    if _pool is None:
-        from concurrent.futures import ThreadPoolExecutor
-
-        _pool = ThreadPoolExecutor(_STAGE_THREADS, thread_name_prefix="aqr-h2d")
+    _pool = _stage_pool()  # a plain copy: nothing to overlap with, the full staging rate
     out = t.empty((n, m), dtype=t.float64, device=dev)  # row j = column j (column-major (m, n))
     stage = t.empty((n, m), dtype=t.float64, pin_memory=True)
     src, dst = A.T, stage.numpy()  # (n, m) C-ordered views
-    nchunks = min(n, 4 * _STAGE_THREADS)
+    nchunks = min(n, 4 * _pool._max_workers)
     bounds = [(k * n) // nchunks for k in range(nchunks + 1)]
     futs = [_pool.submit(np.copyto, dst[b0:b1], src[b0:b1]) for b0, b1 in zip(bounds[:-1], bounds[1:]) if b1 > b0]
     k = 0

@@ -16,11 +16,19 @@ del csr
 Zh = np.asfortranarray(Zd.t().cpu().numpy().T)
 del Zd
 torch.cuda.empty_cache()
-times = []
-for k in range(K + 1):
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    r = aqr.factorize(Zh, op, meth)
-    times.append(time.perf_counter() - t0)
-    del r
-print(" ".join(f"{1e3 * t:.0f}" for t in times), "ms (first = warm-up)", flush=True)
+from paper_1703_10440_b200 import _device as D
+
+# AQR_STAGE_THREADS=a,b,...: repeat the series with these host staging pool sizes
+for threads in [int(x) for x in os.environ.get("AQR_STAGE_THREADS", "0").split(",")]:
+    if threads:
+        D._STAGE_THREADS = threads
+        D._pools.clear()
+    times = []
+    for k in range(K + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = aqr.factorize(Zh, op, meth)
+        times.append(time.perf_counter() - t0)
+        del r
+    print(f"staging threads {D._STAGE_THREADS}:", " ".join(f"{1e3 * t:.0f}" for t in times), "ms (first = warm-up)",
+          flush=True)

@@ -1,6 +1,7 @@
-"""Diagnostics: H2D and D2H bandwidth alone and concurrently (page-locked, 537 MB each)."""
-import torch, time
-n = 537 * 1024 * 1024 // 8
+"""Diagnostics: H2D and D2H bandwidth alone and concurrently (page-locked, 537 MB each;
+`python tools/pcie_duplex.py MB` for another size)."""
+import sys, torch, time
+n = (int(sys.argv[1]) if len(sys.argv) > 1 else 537) * 1024 * 1024 // 8
 h1 = torch.empty(n, dtype=torch.float64).pin_memory(); h2 = torch.empty(n, dtype=torch.float64).pin_memory()
 d1 = torch.empty(n, dtype=torch.float64, device="cuda"); d2 = torch.empty(n, dtype=torch.float64, device="cuda")
 s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()

@@ -12,7 +12,7 @@ print(f"os.cpu_count() = {os.cpu_count()}, Z {Z.nbytes / 1e9:.1f} GB", flush=Tru
 bounds = np.arange(0, n + 1, 8)
 for threads in (8, 16, 32):
     D._STAGE_THREADS = threads
-    D._pool = None
+    D._pools.clear()
     for rep in range(2):
         t0 = time.perf_counter()
         st = D.StagedHost(Z, bounds)
