@@ -189,3 +189,22 @@ def test_diffusion7_symmetric_and_diagonally_dominant():
     off = np.asarray(abs(A).sum(axis=1)).ravel() - d
     assert np.all(d > off)
     assert ip[-1] == 7 * 12 ** 3 - 6 * 12 ** 2
+
+
+def test_stage_pool_size_follows_input_width():
+    """Host staging threads: throttled for wide (compute-bound) inputs, the
+    full pool for narrow ones and plain copies; AQR_STAGE_THREADS overrides."""
+    from paper_1703_10440_b200 import _device as D
+
+    cores = os.cpu_count() or 4
+    old = D._STAGE_THREADS
+    try:
+        D._STAGE_THREADS = 0
+        assert D._stage_pool(256)._max_workers == max(2, min(4, cores))
+        assert D._stage_pool(64)._max_workers == max(2, min(8, cores))
+        assert D._stage_pool()._max_workers == max(2, min(8, cores))
+        assert D._stage_pool(256) is D._stage_pool(1024)  # one pool per size
+        D._STAGE_THREADS = 3
+        assert D._stage_pool(256)._max_workers == 3 and D._stage_pool(8)._max_workers == 3
+    finally:
+        D._STAGE_THREADS = old
