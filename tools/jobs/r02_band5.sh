@@ -1,4 +1,4 @@
-# cp.async-staged k = 1 step for long banded rows vs the gather step (experiments build).
+# cp.async-staged k = 1 step for long banded rows (intermediate build: measured, not kept) vs the gather step.
 set -u
 O=gpurun_out
 mkdir -p $O

@@ -1,4 +1,5 @@
-# HP: just-in-time X catch-up (AQR_X_JIT) vs all stored columns every window.
+# HP: just-in-time X catch-up (AQR_X_JIT, a knob of an intermediate build: measured, not kept -- profiles/r02/ab_xjit.txt)
+# vs all stored columns every window.
 set -u
 O=gpurun_out
 mkdir -p $O
