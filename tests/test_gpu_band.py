@@ -179,3 +179,36 @@ def test_breakdown_same(aqr):
             aqr.mgs_ha(Z, aqr.CsrSpdOperator(*csr, banded=banded), "row")
         errs.append((ei.value.column, ei.value.value))
     assert errs[0] == errs[1]
+
+
+@pytest.mark.parametrize("name", ["lap5", "diff7", "st27", "st27b"])
+def test_padded_leading_dimensions_and_canaries(aqr, name):
+    """C ABI products with ldx, ldy > m: results unchanged, the padding rows of Y untouched
+    (compute-sanitizer is not available on the GPU pool; this is the bounds check)."""
+    import ctypes
+
+    import torch
+
+    from paper_1703_10440_b200 import _device as D
+    from paper_1703_10440_b200 import _lib
+
+    make, _, _ = CASES[name]
+    csr = make()
+    band, plain = aqr.CsrSpdOperator(*csr), aqr.CsrSpdOperator(*csr, banded=False)
+    m = band.dim
+    L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(21)
+    for k, pad in ((1, 0), (1, 5), (3, 7), (8, 16), (11, 3)):
+        ld = m + pad
+        X = torch.randn((k, ld), generator=g, device="cuda", dtype=torch.float64)  # column j = row j
+        X[:, m:] = float("nan")  # padding rows of X must never be read into a result
+        out = []
+        for op in (band, plain):
+            Y = torch.full((k, ld + 4), -7.5, device="cuda", dtype=torch.float64)
+            _lib.check(L.aqr_op_apply(ctypes.byref(op._native()), k, X.data_ptr(), ld, Y.data_ptr(), ld + 4,
+                                      D.stream_ptr()), "aqr_op_apply")
+            torch.cuda.synchronize()
+            assert bool((Y[:, m:] == -7.5).all()), (name, k, pad)
+            assert bool(torch.isfinite(Y[:, :m]).all()), (name, k, pad)
+            out.append(Y[:, :m].clone())
+        assert torch.equal(out[0], out[1]), (name, k, pad)
